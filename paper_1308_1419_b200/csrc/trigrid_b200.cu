@@ -1,0 +1,951 @@
+// trigrid_b200.cu -- host side of the C-ABI (include/trigrid_b200.h):
+// validation with the reference's error classes, closed-form DispatchStats,
+// lambda-range sharding, launch planning for the GRID and SPAN kernels, and
+// the pipelined host-buffer drop-ins.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/trigrid_b200.h"
+#include "tg_kernels.cuh"
+
+using namespace tg;
+
+namespace {
+
+constexpr uint64_t kMaxElems = uint64_t{1} << 20;  // tri.hpp:11
+
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+
+tg_status fail(tg_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define TG_CUDA(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            (void)cudaGetLastError();                                                   \
+            return fail(e_ == cudaErrorMemoryAllocation ? TG_ENOMEM : TG_ECUDA,         \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));            \
+        }                                                                               \
+    } while (0)
+
+#define TG_TRY(expr)                   \
+    do {                               \
+        tg_status s_ = (expr);         \
+        if (s_ != TG_OK) return s_;    \
+    } while (0)
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+bool is_ltm(tg_strategy s) { return s >= TG_LTM_X && s <= TG_LTM_EXACT; }
+int ltm_engine(tg_strategy s) {
+    switch (s) {
+        case TG_LTM_X: return kNative;
+        case TG_LTM_N: return kNewton;
+        case TG_LTM_R: return kReciprocal;
+        default: return kExact;
+    }
+}
+
+// ProblemSize (tri.cpp:9-15) plus the per-strategy constructors' checks.
+tg_status validate_problem(tg_strategy s, uint64_t n, uint32_t rho) {
+    if (n == 0) return fail(TG_EINVAL, "ProblemSize: N must be >= 1");
+    if (n > kMaxElems) return fail(TG_EINVAL, "ProblemSize: N exceeds the 2^20 cap");
+    if (rho == 0) return fail(TG_EINVAL, "ProblemSize: rho must be >= 1");
+    if ((int)s < 0 || (int)s > (int)TG_REC) return fail(TG_EINVAL, "make_strategy: unknown strategy kind");
+    if (s == TG_RB && n < 2) return fail(TG_EINVAL, "rb_rect: N must be >= 2");
+    if (s == TG_REC) {
+        uint64_t m;
+        uint32_t k;
+        if (!rec_decompose(n, rho, &m, &k))
+            return fail(TG_EINVAL, "rec: N is not m*2^k with m a multiple of rho");
+    }
+    return TG_OK;
+}
+
+// ------------------------------------------------------------ sharding
+
+// Block-row bounds of G lambda-range shards: rows[g] is the block row whose
+// start T(r) is nearest to g*T(nb)/G.
+std::vector<uint64_t> shard_rows(uint64_t nb, uint32_t G) {
+    std::vector<uint64_t> rows(G + 1, 0);
+    const uint64_t total = tri(nb);
+    rows[G] = nb;
+    for (uint32_t g = 1; g < G; ++g) {
+        const uint64_t target = (uint64_t)((unsigned __int128)total * g / G);
+        const uint64_t r = fix_row(ltm_row_guess(target, kExact, true), target, true);
+        const uint64_t lo = tri(r), hi = tri(r + 1);
+        uint64_t b = (target - lo <= hi - target) ? r : r + 1;
+        b = std::min(std::max(b, rows[g - 1]), nb);
+        rows[g] = b;
+    }
+    return rows;
+}
+
+// --------------------------------------------------- closed-form stats
+
+// threads filtered inside the surviving tiles of block rows [b0, b1)
+// (process_block FullTile/DiagTile, engine.cpp:26-55).
+uint64_t tile_threads_discarded(uint64_t n, uint64_t rho, uint64_t b0, uint64_t b1) {
+    const uint64_t nb = ceil_div(n, rho);
+    uint64_t t = 0;
+    const uint64_t full_rows_end = std::min(b1, nb - 1);
+    if (full_rows_end > b0) t += (full_rows_end - b0) * (rho * (rho - 1) / 2);
+    if (b1 == nb && nb - 1 >= b0) {  // last block row, r valid cell rows
+        const uint64_t b = nb - 1, r = n - rho * b;
+        uint64_t diag = 0;
+        for (uint64_t dy = 0; dy < r; ++dy) diag += rho - dy - 1;
+        if (r < rho) diag += rho * (rho - r);
+        const uint64_t full = (r < rho) ? b * rho * (rho - r) : 0;
+        t += diag + full;
+    }
+    return t;
+}
+
+struct RecPlan {
+    uint64_t m;
+    uint32_t k;
+};
+
+tg_status stats_for(tg_strategy s, uint64_t n, uint32_t rho, uint32_t shard, uint32_t shards,
+                    tg_dispatch_stats* st) {
+    TG_TRY(validate_problem(s, n, rho));
+    *st = tg_dispatch_stats{0, 0, 0, 0};
+    const uint64_t nb = ceil_div(n, rho);
+    const uint32_t G = shards == 0 ? 1 : shards;
+    if (shard >= G) return fail(TG_EINVAL, "shard_index must be < shard_count");
+    if (G > 1 && !(s == TG_BB || is_ltm(s)))
+        return fail(TG_EINVAL, "lambda-range sharding applies to bb and ltm-* only");
+    if (s == TG_BB || is_ltm(s)) {
+        const auto rows = shard_rows(nb, G);
+        const uint64_t b0 = rows[shard], b1 = rows[shard + 1];
+        if (s == TG_BB) {
+            const uint64_t W = b1, H = b1 - b0;
+            st->blocks_launched = W * H;
+            // sum over grid rows y in [b0, b1) of the W - 1 - y blocks with x > y
+            st->blocks_discarded = H * (H - (H > 0 ? 1 : 0)) / 2;
+        } else {
+            const uint64_t L = tri(b1) - tri(b0);
+            const uint64_t side = L ? ceil_sqrt(L) : 0;
+            st->blocks_launched = side * side;
+            st->blocks_discarded = side * side - L;
+        }
+        st->threads_discarded = (b1 > b0) ? tile_threads_discarded(n, rho, b0, b1) : 0;
+        return TG_OK;
+    }
+    if (s == TG_UTM) {
+        const uint64_t pairs = tri_nd(n), tpb = (uint64_t)rho * rho;
+        const uint64_t blocks = pairs == 0 ? 1 : ceil_div(pairs, tpb);
+        st->blocks_launched = blocks;
+        st->threads_discarded = blocks * tpb - pairs;
+        return TG_OK;
+    }
+    if (s == TG_RB) {
+        const uint64_t w = (n % 2 == 0) ? n / 2 : (n + 1) / 2, h = (n % 2 == 0) ? n + 1 : n;
+        const uint64_t gx = ceil_div(w, rho), gy = ceil_div(h, rho);
+        st->blocks_launched = gx * gy;
+        st->threads_discarded = gx * gy * rho * rho - w * h;
+        return TG_OK;
+    }
+    // REC
+    uint64_t m;
+    uint32_t k;
+    rec_decompose(n, rho, &m, &k);
+    uint64_t launched = 0;
+    for (uint32_t level = 1; level <= k; ++level) {
+        const uint64_t side = m << (level - 1), sb = side / rho;
+        launched += sb * sb * (1ull << (k - level));
+    }
+    const uint64_t sb = m / rho, tris = 1ull << k;
+    launched += sb * sb * tris;
+    st->blocks_launched = launched;
+    st->blocks_discarded = tris * (sb * (sb - 1) / 2);
+    st->threads_discarded = tris * sb * ((uint64_t)rho * (rho - 1) / 2);
+    return TG_OK;
+}
+
+// ------------------------------------------------------- device context
+
+constexpr unsigned kFlagRing = 1024;
+
+struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+struct DeviceCtx {
+    std::mutex mu;
+    bool init = false;
+    int dev = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;       // internal compute stream (host drop-ins)
+    cudaStream_t copy_stream = nullptr;  // D2H pipeline
+    unsigned int* flags = nullptr;       // classify verdicts (ring, one per launch)
+    unsigned flag_next = 0;
+    unsigned long long* scratch = nullptr;  // [0] sink [1] bad [2] first [3] hits
+    Buf bufs[4];
+    cudaEvent_t ev[34];
+};
+
+DeviceCtx g_ctx[64];
+
+unsigned int* next_flag(DeviceCtx* c) {
+    const unsigned slot = __atomic_fetch_add(&c->flag_next, 1u, __ATOMIC_RELAXED) % kFlagRing;
+    return c->flags + slot;
+}
+
+tg_status ensure_buf(Buf& b, size_t bytes) {
+    if (b.cap >= bytes) return TG_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    TG_CUDA(cudaMalloc(&b.p, std::max<size_t>(bytes, 256)));
+    b.cap = std::max<size_t>(bytes, 256);
+    return TG_OK;
+}
+
+tg_status get_ctx(int device, DeviceCtx** out) {
+    int dev = device;
+    if (dev < 0) TG_CUDA(cudaGetDevice(&dev));
+    if (dev >= 64) return fail(TG_EINVAL, "device ordinal out of range");
+    TG_CUDA(cudaSetDevice(dev));
+    DeviceCtx& c = g_ctx[dev];
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (!c.init) {
+        c.dev = dev;
+        TG_CUDA(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
+        TG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        TG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+        TG_CUDA(cudaMalloc(&c.flags, kFlagRing * sizeof(unsigned int)));
+        TG_CUDA(cudaMalloc(&c.scratch, 256));
+        for (auto& e : c.ev) TG_CUDA(cudaEventCreate(&e));
+        c.init = true;
+    }
+    *out = &c;
+    return TG_OK;
+}
+
+// --------------------------------------------------------- span planning
+
+int span_slots() {
+    static int p = [] {
+        const char* e = std::getenv("TG_SPAN_SLOTS");
+        int v = e ? std::atoi(e) : 1;
+        return (v == 2) ? 2 : 1;
+    }();
+    return p;
+}
+
+bool span_eligible(tg_strategy s, uint32_t rho) {
+    return (s == TG_BB || is_ltm(s) || s == TG_REC) && rho % 4 == 0 && rho <= 128;
+}
+
+// Geometry for block rows [b0, b1).
+tg_status plan_span(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64_t b1, uint32_t C,
+                    SpanGeom* g) {
+    std::memset(g, 0, sizeof(*g));
+    g->rho = rho;
+    g->C = C;
+    g->n = n;
+    g->b0 = b0;
+    const uint64_t nb = ceil_div(n, rho);
+    if (s == TG_BB) {
+        g->strat = kSpanBB;
+        g->W = b1;
+        g->vb_count = b1 * (b1 - b0);
+        g->units = ceil_div(g->vb_count, C);
+    } else if (is_ltm(s)) {
+        g->strat = kSpanLTM;
+        g->engine = ltm_engine(s);
+        g->lam0 = tri(b0);
+        g->lam1 = tri(b1);
+        const uint64_t L = g->lam1 - g->lam0;
+        const uint64_t side = L ? ceil_sqrt(L) : 0;
+        g->vb_count = side * side;  // balanced grid (tri.cpp:23-26) incl. padding
+        g->units = ceil_div(g->vb_count, C);
+    } else if (s == TG_REC) {
+        if (b0 != 0 || b1 != nb) return fail(TG_EINVAL, "rec cannot be sharded");
+        g->strat = kSpanREC;
+        uint64_t m;
+        uint32_t k;
+        rec_decompose(n, rho, &m, &k);
+        g->m = m;
+        uint64_t unit = 0;
+        int p = 0;
+        for (uint32_t level = 1; level <= k; ++level, ++p) {
+            const uint64_t side = m << (level - 1), sb = side / rho;
+            g->pass[p] = RecPass{unit, sb * sb * (1ull << (k - level)), sb, side, level};
+            unit += ceil_div(g->pass[p].vb_count, C);
+        }
+        const uint64_t sb = m / rho;
+        g->pass[p] = RecPass{unit, sb * sb * (1ull << k), sb, m, 0};
+        unit += ceil_div(g->pass[p].vb_count, C);
+        g->npass = p + 1;
+        g->units = unit;
+        g->vb_count = 0;
+    } else {
+        return fail(TG_EINVAL, "span mode supports bb, ltm-* and rec");
+    }
+    return TG_OK;
+}
+
+uint64_t span_grid(const SpanGeom& g, bool persistent, int sms, int occ) {
+    const uint64_t need = ceil_div(g.units, kWarpsPerCta);
+    if (need == 0) return 0;
+    uint64_t grid = need;
+    if (persistent) grid = std::min<uint64_t>(need, (uint64_t)sms * std::max(occ, 1));
+    return std::min<uint64_t>(grid, 0x7fffffffull);
+}
+
+template <int D, int P>
+tg_status launch_span_edm_t(const SpanGeom& g, OutWin ow, const float* pts, float* out,
+                            const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
+    static int occ = -1;
+    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_edm_kernel<D, P>, kWarpsPerCta * 32, 0);
+    const uint64_t grid = span_grid(g, persistent, sms, occ);
+    if (!grid) return TG_OK;
+    span_edm_kernel<D, P><<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, ow, pts, out, flag);
+    ++g_launches;
+    TG_CUDA(cudaGetLastError());
+    return TG_OK;
+}
+
+template <int P>
+tg_status launch_span_edm_p(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
+                            const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
+    switch (d) {
+        case 1: return launch_span_edm_t<1, P>(g, ow, pts, out, flag, st, persistent, sms);
+        case 2: return launch_span_edm_t<2, P>(g, ow, pts, out, flag, st, persistent, sms);
+        case 3: return launch_span_edm_t<3, P>(g, ow, pts, out, flag, st, persistent, sms);
+        case 4: return launch_span_edm_t<4, P>(g, ow, pts, out, flag, st, persistent, sms);
+    }
+    return fail(TG_EINVAL, "span EDM supports d in [1, 4]");
+}
+
+tg_status launch_span_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
+                          const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
+    return span_slots() == 2 ? launch_span_edm_p<2>(d, g, ow, pts, out, flag, st, persistent, sms)
+                             : launch_span_edm_p<1>(d, g, ow, pts, out, flag, st, persistent, sms);
+}
+
+tg_status launch_classify(const float* pts, uint64_t count, unsigned int* flag, cudaStream_t st, int sms) {
+    TG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned int), st));
+    const uint64_t blocks = std::min<uint64_t>(ceil_div(count, 256), (uint64_t)sms * 4);
+    classify_points_kernel<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, st>>>(pts, count, flag);
+    ++g_launches;
+    TG_CUDA(cudaGetLastError());
+    return TG_OK;
+}
+
+template <int P>
+tg_status launch_span_write_p(const SpanGeom& g, OutWin ow, uint32_t* out, cudaStream_t st,
+                              bool persistent, int sms) {
+    static int occ = -1;
+    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_write_kernel<P>, kWarpsPerCta * 32, 0);
+    const uint64_t grid = span_grid(g, persistent, sms, occ);
+    if (!grid) return TG_OK;
+    span_write_kernel<P><<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, ow, out);
+    ++g_launches;
+    TG_CUDA(cudaGetLastError());
+    return TG_OK;
+}
+
+tg_status launch_span_write(const SpanGeom& g, OutWin ow, uint32_t* out, cudaStream_t st,
+                            bool persistent, int sms) {
+    return span_slots() == 2 ? launch_span_write_p<2>(g, ow, out, st, persistent, sms)
+                             : launch_span_write_p<1>(g, ow, out, st, persistent, sms);
+}
+
+// --------------------------------------------------------- grid planning
+
+std::vector<GridGeom> plan_grid(tg_strategy s, uint64_t n, uint32_t rho) {
+    std::vector<GridGeom> passes;
+    GridGeom g{};
+    g.rho = rho;
+    g.n = n;
+    const uint64_t nb = ceil_div(n, rho);
+    if (s == TG_BB) {
+        g.strat = kGridBB;
+        g.blocks_x = nb;
+        g.vb_count = nb * nb;
+        passes.push_back(g);
+    } else if (is_ltm(s)) {
+        g.strat = kGridLTM;
+        g.engine = ltm_engine(s);
+        const uint64_t side = ceil_sqrt(tri(nb));
+        g.blocks_x = side;
+        g.vb_count = side * side;
+        g.lam_count = tri(nb);
+        passes.push_back(g);
+    } else if (s == TG_UTM) {
+        g.strat = kGridUTM;
+        g.engine = kNewton;  // parse_strategy("utm") (strategies.cpp:24)
+        g.pairs = tri_nd(n);
+        g.disc_base = (2 * n - 1) * (2 * n - 1);
+        const uint64_t tpb = (uint64_t)rho * rho;
+        g.vb_count = g.pairs == 0 ? 1 : ceil_div(g.pairs, tpb);
+        g.blocks_x = g.vb_count;
+        passes.push_back(g);
+    } else if (s == TG_RB) {
+        g.strat = kGridRB;
+        const uint64_t w = (n % 2 == 0) ? n / 2 : (n + 1) / 2, h = (n % 2 == 0) ? n + 1 : n;
+        g.blocks_x = ceil_div(w, rho);
+        g.vb_count = g.blocks_x * ceil_div(h, rho);
+        passes.push_back(g);
+    } else {  // REC: k square passes + 1 diagonal pass, one launch each
+        uint64_t m;
+        uint32_t k;
+        rec_decompose(n, rho, &m, &k);
+        g.m = m;
+        for (uint32_t level = 1; level <= k; ++level) {
+            GridGeom p = g;
+            p.strat = kGridRECSq;
+            p.side = m << (level - 1);
+            p.sb = p.side / rho;
+            p.blocks_x = p.sb;
+            p.vb_count = p.sb * p.sb * (1ull << (k - level));
+            passes.push_back(p);
+        }
+        GridGeom p = g;
+        p.strat = kGridRECDiag;
+        p.side = m;
+        p.sb = m / rho;
+        p.blocks_x = p.sb;
+        p.vb_count = p.sb * p.sb * (1ull << k);
+        passes.push_back(p);
+    }
+    return passes;
+}
+
+template <class Body>
+tg_status launch_grid(const std::vector<GridGeom>& passes, Body body, cudaStream_t st) {
+    for (const GridGeom& g : passes) {
+        if (g.vb_count == 0) continue;
+        const uint32_t threads = std::min<uint32_t>(g.rho * g.rho, 1024);
+        const uint64_t blocks = std::min<uint64_t>(g.vb_count, 0x7fffffffull);
+        grid_kernel<Body><<<(unsigned)blocks, threads, 0, st>>>(g, body);
+        ++g_launches;
+        TG_CUDA(cudaGetLastError());
+    }
+    return TG_OK;
+}
+
+// ------------------------------------------------------------- timing
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t st;
+    bool on;
+    Timer(cudaStream_t s, bool enable) : st(s), on(enable) {
+        if (on) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, st);
+        }
+    }
+    tg_status finish(tg_dispatch_stats* stats) {
+        if (!on) return TG_OK;
+        TG_CUDA(cudaEventRecord(b, st));
+        TG_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        TG_CUDA(cudaEventElapsedTime(&ms, a, b));
+        if (stats) stats->wall_time_ns = (uint64_t)std::llround((double)ms * 1e6);
+        return TG_OK;
+    }
+    ~Timer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+tg_launch_opts default_opts() {
+    tg_launch_opts o;
+    tg_launch_opts_init(&o);
+    return o;
+}
+
+bool resolve_span(const tg_launch_opts& o, tg_strategy s, uint32_t rho, bool body_ok) {
+    if (o.mode == TG_MODE_GRID) return false;
+    const bool ok = body_ok && span_eligible(s, rho);
+    return o.mode == TG_MODE_SPAN ? true : ok;
+}
+
+}  // namespace
+
+// ======================================================================
+extern "C" {
+
+void tg_launch_opts_init(tg_launch_opts* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->device = -1;
+    o->mode = TG_MODE_AUTO;
+    o->sentinel = ~0ull;
+}
+
+const char* tg_last_error(void) { return g_err.c_str(); }
+int tg_api_version(void) { return TG_API_VERSION; }
+uint64_t tg_last_launch_count(void) { return g_launches; }
+
+uint64_t tg_tri_count(uint64_t n, int with_diag) { return tri_count(n, with_diag != 0); }
+
+tg_status tg_tri_linear_index(uint64_t i, uint64_t j, uint64_t* out) {
+    if (j > i) return fail(TG_ERANGE, "tri_linear_index: j > i is outside the lower triangle");
+    *out = i * (i + 1) / 2 + j;
+    return TG_OK;
+}
+
+tg_status tg_grid_side_balanced(uint64_t n, uint64_t* out) {
+    if (n == 0) return fail(TG_EINVAL, "grid_side_balanced: n must be >= 1");
+    *out = ceil_sqrt(tri(n));
+    return TG_OK;
+}
+
+uint64_t tg_isqrt(uint64_t v) { return isqrt(v); }
+float tg_fast_inv_sqrt(float x, int iterations) { return fast_inv_sqrt(x, iterations); }
+float tg_rsqrt_single(float x) { return 1.0f / std::sqrt(x); }
+
+tg_status tg_sqrt_via(int engine, double x, double* out) {
+    if (std::isnan(x) || std::isinf(x) || x < 0.0)
+        return fail(TG_EINVAL, "sqrt_via: x must be finite and non-negative");
+    switch (engine) {
+        case kNative: *out = (double)std::sqrt((float)x); return TG_OK;
+        case kNewton:
+            if (x == 0.0) return fail(TG_EINVAL, "sqrt_via: NewtonRaphson requires x > 0");
+            *out = (double)engine_sqrt(kNewton, (float)x);
+            return TG_OK;
+        case kReciprocal:
+            if (x == 0.0) return fail(TG_EINVAL, "sqrt_via: Reciprocal requires x > 0");
+            *out = (double)engine_sqrt(kReciprocal, (float)x);
+            return TG_OK;
+        case kExact:
+            if (x != std::floor(x) || x > 0x1p53)
+                return fail(TG_EINVAL, "sqrt_via: ExactInteger requires an integral x");
+            *out = (double)isqrt((uint64_t)x);
+            return TG_OK;
+    }
+    return fail(TG_EINVAL, "sqrt_via: unknown engine variant");
+}
+
+tg_status tg_ltm_map(uint64_t lambda, int engine, int with_diag, uint64_t* i, uint64_t* j) {
+    if (engine < 0 || engine > 3) return fail(TG_EINVAL, "ltm_map: unknown engine");
+    const Coord c = ltm_map(lambda, engine, with_diag != 0);
+    *i = c.i;
+    *j = c.j;
+    return TG_OK;
+}
+
+int tg_bb_map(uint64_t x, uint64_t y, uint64_t* i, uint64_t* j) {
+    if (x > y) return 0;
+    *i = y;
+    *j = x;
+    return 1;
+}
+
+tg_status tg_utm_map(uint64_t k, uint64_t n, int engine, uint64_t* a, uint64_t* b) {
+    if (n < 2 || k >= tri_nd(n)) return fail(TG_ERANGE, "utm_map: k outside [0, N(N-1)/2)");
+    const Coord p = utm_pair(k, n, (2 * n - 1) * (2 * n - 1), engine);
+    *a = p.i;
+    *b = p.j;
+    return TG_OK;
+}
+
+tg_status tg_rb_rect(uint64_t n, uint64_t* w, uint64_t* h) {
+    if (n < 2) return fail(TG_EINVAL, "rb_rect: N must be >= 2");
+    if (n % 2 == 0) {
+        *w = n / 2;
+        *h = n + 1;
+    } else {
+        *w = (n + 1) / 2;
+        *h = n;
+    }
+    return TG_OK;
+}
+
+int tg_rb_map(uint64_t tx, uint64_t ty, uint64_t n, uint64_t* i, uint64_t* j) {
+    Coord c;
+    if (!rb_map(tx, ty, n, &c)) return 0;
+    *i = c.i;
+    *j = c.j;
+    return 1;
+}
+
+int tg_rec_decompose(uint64_t n, uint32_t rho, uint64_t* m, uint32_t* k) {
+    if (rho == 0) return 0;
+    return rec_decompose(n, rho, m, k) ? 1 : 0;
+}
+
+tg_status tg_count_wasted(tg_strategy s, uint64_t n, uint64_t* out) {
+    if (n == 0) return fail(TG_EINVAL, "count_wasted: n must be >= 1");
+    if (s == TG_BB) {
+        *out = n * (n - 1) / 2;
+        return TG_OK;
+    }
+    if (is_ltm(s)) {
+        const uint64_t side = ceil_sqrt(tri(n));
+        *out = side * side - tri(n);
+        return TG_OK;
+    }
+    return fail(TG_EINVAL, "count_wasted: no closed form for this strategy");
+}
+
+tg_status tg_improvement_model(double beta, double tau, double n, double* out) {
+    if (!(beta > 0.0) || !(tau > 0.0))
+        return fail(TG_EINVAL, "improvement_model: beta and tau must be positive");
+    if (!(n >= 1.0)) return fail(TG_EINVAL, "improvement_model: n must be >= 1");
+    *out = 2.0 * beta * n * n / (tau * n * n + tau * n);
+    return TG_OK;
+}
+
+tg_status tg_parse_strategy(const char* name, tg_strategy* out) {
+    static const char* names[] = {"bb", "ltm-x", "ltm-n", "ltm-r", "ltm-exact", "utm", "rb", "rec"};
+    if (name)
+        for (int t = 0; t < 8; ++t)
+            if (std::strcmp(name, names[t]) == 0) {
+                *out = (tg_strategy)t;
+                return TG_OK;
+            }
+    return fail(TG_EINVAL, std::string("unknown strategy '") + (name ? name : "") + "'");
+}
+
+tg_status tg_dispatch_stats_for(tg_strategy s, uint64_t n, uint32_t rho, uint32_t shard_index,
+                                uint32_t shard_count, tg_dispatch_stats* out) {
+    return stats_for(s, n, rho, shard_index, shard_count, out);
+}
+
+tg_status tg_shard_rows(uint64_t n, uint32_t rho, uint32_t shard_count, uint64_t* rows) {
+    if (n == 0 || rho == 0 || shard_count == 0) return fail(TG_EINVAL, "tg_shard_rows: bad arguments");
+    const auto r = shard_rows(ceil_div(n, rho), shard_count);
+    std::copy(r.begin(), r.end(), rows);
+    return TG_OK;
+}
+
+tg_status tg_shard_elems(uint64_t n, uint32_t rho, uint32_t shard_index, uint32_t shard_count,
+                         int with_diag, uint64_t* begin, uint64_t* end) {
+    const uint32_t G = shard_count == 0 ? 1 : shard_count;
+    if (n == 0 || rho == 0 || shard_index >= G) return fail(TG_EINVAL, "tg_shard_elems: bad arguments");
+    const auto r = shard_rows(ceil_div(n, rho), G);
+    const uint64_t i0 = std::min<uint64_t>(n, r[shard_index] * rho);
+    const uint64_t i1 = std::min<uint64_t>(n, r[shard_index + 1] * rho);
+    *begin = tri_count(i0, with_diag != 0);
+    *end = tri_count(i1, with_diag != 0);
+    return TG_OK;
+}
+
+tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uint32_t rho,
+                    const float* pts, void* out, const tg_launch_opts* opts,
+                    tg_dispatch_stats* stats) {
+    g_launches = 0;
+    const tg_launch_opts o = opts ? *opts : default_opts();
+    TG_TRY(validate_problem(s, n, rho));
+    const uint32_t G = o.shard_count == 0 ? 1 : o.shard_count;
+    tg_dispatch_stats st_local;
+    TG_TRY(stats_for(s, n, rho, o.shard_index, G, &st_local));
+    if (kernel == TG_KERNEL_EDM) {
+        if (d < 1) return fail(TG_EINVAL, "launch_edm: features must be >= 1");
+        if (!pts || !out) return fail(TG_EINVAL, "launch: EDM kernel needs points and an output buffer");
+        if (reinterpret_cast<uintptr_t>(pts) % 16 != 0)
+            return fail(TG_EINVAL, "launch_edm: device points must be 16-byte aligned");
+    }
+    if ((kernel == TG_KERNEL_WRITE || kernel == TG_KERNEL_COUNT) && !out)
+        return fail(TG_EINVAL, "launch: output buffer is NULL");
+    if (kernel == TG_KERNEL_EDM || kernel == TG_KERNEL_WRITE) {
+        if (reinterpret_cast<uintptr_t>(out) % 16 != 0)
+            return fail(TG_EINVAL, "launch: device output must be 16-byte aligned");
+    }
+    DeviceCtx* c;
+    TG_TRY(get_ctx(o.device, &c));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(o.stream);
+    const bool body_span = (kernel == TG_KERNEL_EDM && d <= 4) || kernel == TG_KERNEL_WRITE;
+    const bool span = resolve_span(o, s, rho, body_span);
+    if (span && !(body_span && span_eligible(s, rho)))
+        return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec, rho % 4 == 0 and an edm (d<=4) or write body");
+    if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode (bb/ltm-*)");
+
+    Timer timer(st, !o.async);
+    if (span) {
+        const uint64_t nb = ceil_div(n, rho);
+        const auto rows = shard_rows(nb, G);
+        const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
+        SpanGeom g;
+        const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * span_slots()) / rho);
+        TG_TRY(plan_span(s, n, rho, b0, b1, C, &g));
+        OutWin ow{tri(std::min<uint64_t>(n, b0 * rho)), tri(std::min<uint64_t>(n, b1 * rho))};
+        if (kernel == TG_KERNEL_EDM) {
+            unsigned int* flag = next_flag(c);
+            TG_TRY(launch_classify(pts, n * d, flag, st, c->sms));
+            TG_TRY(launch_span_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms));
+        } else {
+            TG_TRY(launch_span_write(g, ow, static_cast<uint32_t*>(out), st, o.persistent != 0, c->sms));
+        }
+    } else {
+        const auto passes = plan_grid(s, n, rho);
+        switch (kernel) {
+            case TG_KERNEL_EDM:
+                TG_TRY(launch_grid(passes, EdmBody{pts, static_cast<float*>(out), d}, st));
+                break;
+            case TG_KERNEL_WRITE:
+                TG_TRY(launch_grid(passes, WriteBody{static_cast<uint32_t*>(out)}, st));
+                break;
+            case TG_KERNEL_COUNT:
+                TG_TRY(launch_grid(passes, CountBody{static_cast<uint32_t*>(out)}, st));
+                break;
+            case TG_KERNEL_DUMMY: {
+                auto* sink = o.sink ? static_cast<unsigned long long*>(o.sink) : c->scratch;
+                TG_TRY(launch_grid(passes, DummyBody{sink, o.sentinel}, st));
+                break;
+            }
+            default:
+                return fail(TG_EINVAL, "launch: unknown kernel kind");
+        }
+    }
+    TG_TRY(timer.finish(&st_local));
+    if (stats) *stats = st_local;
+    return TG_OK;
+}
+
+tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spheres, float r_max,
+                     uint32_t* bits, uint64_t* hits, const tg_launch_opts* opts,
+                     tg_dispatch_stats* stats) {
+    g_launches = 0;
+    const tg_launch_opts o = opts ? *opts : default_opts();
+    TG_TRY(validate_problem(s, n, rho));
+    if (!spheres || !bits || !hits) return fail(TG_EINVAL, "collide: NULL buffer");
+    if (reinterpret_cast<uintptr_t>(spheres) % 16 != 0)
+        return fail(TG_EINVAL, "collide: spheres must be 16-byte aligned");
+    const uint32_t G = o.shard_count == 0 ? 1 : o.shard_count;
+    tg_dispatch_stats st_local;
+    TG_TRY(stats_for(s, n, rho, o.shard_index, G, &st_local));
+    DeviceCtx* c;
+    TG_TRY(get_ctx(o.device, &c));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(o.stream);
+    const bool span = resolve_span(o, s, rho, true);
+    if (span && !span_eligible(s, rho)) return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec and rho % 4 == 0");
+    if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode (bb/ltm-*)");
+    uint64_t p0, p1;
+    TG_TRY(tg_shard_elems(n, rho, o.shard_index, G, 0, &p0, &p1));
+    Timer timer(st, !o.async);
+    TG_CUDA(cudaMemsetAsync(hits, 0, sizeof(uint64_t), st));
+    if (span) {
+        const uint64_t nb = ceil_div(n, rho);
+        const auto rows = shard_rows(nb, G);
+        SpanGeom g;
+        TG_TRY(plan_span(s, n, rho, rows[o.shard_index], rows[o.shard_index + 1],
+                         std::max<uint32_t>(1, 128 / rho), &g));
+        const uint64_t grid = span_grid(g, o.persistent != 0, c->sms, 8);
+        if (grid) {
+            span_collide_kernel<<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(
+                g, p0, p1, reinterpret_cast<const float4*>(spheres), r_max, bits,
+                reinterpret_cast<unsigned long long*>(hits));
+            ++g_launches;
+            TG_CUDA(cudaGetLastError());
+        }
+    } else {
+        TG_CUDA(cudaMemsetAsync(bits, 0, ceil_div(p1 - p0, 32) * 4, st));
+        TG_TRY(launch_grid(plan_grid(s, n, rho),
+                           CollideBody{reinterpret_cast<const float4*>(spheres), r_max, bits,
+                                       reinterpret_cast<unsigned long long*>(hits)},
+                           st));
+    }
+    TG_TRY(timer.finish(&st_local));
+    if (stats) *stats = st_local;
+    return TG_OK;
+}
+
+tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint32_t d,
+                               uint32_t rho, float* out, const tg_launch_opts* opts,
+                               tg_dispatch_stats* stats) {
+    g_launches = 0;
+    const tg_launch_opts o = opts ? *opts : default_opts();
+    TG_TRY(validate_problem(s, n, rho));
+    if (d < 1 || d > 4) return fail(TG_EINVAL, "launch_edm: features must be in [1, 4]");
+    if (!pts || !out) return fail(TG_EINVAL, "launch: EDM kernel needs points and an output buffer");
+    const uint32_t G = o.shard_count == 0 ? 1 : o.shard_count;
+    tg_dispatch_stats st_local;
+    TG_TRY(stats_for(s, n, rho, o.shard_index, G, &st_local));
+    DeviceCtx* c;
+    TG_TRY(get_ctx(o.device, &c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = o.stream ? reinterpret_cast<cudaStream_t>(o.stream) : c->stream;
+    const bool span = resolve_span(o, s, rho, true);
+    if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode (bb/ltm-*)");
+    if (span && !span_eligible(s, rho)) return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec and rho % 4 == 0");
+
+    const uint64_t nb = ceil_div(n, rho);
+    const auto rows = shard_rows(nb, G);
+    const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
+    const uint64_t eb = tri(std::min<uint64_t>(n, b0 * rho)), ee = tri(std::min<uint64_t>(n, b1 * rho));
+    const uint64_t elems = ee - eb;
+    TG_TRY(ensure_buf(c->bufs[0], n * d * sizeof(float)));
+    TG_TRY(ensure_buf(c->bufs[1], elems * sizeof(float)));
+    float* d_pts = static_cast<float*>(c->bufs[0].p);
+    float* d_out = static_cast<float*>(c->bufs[1].p);
+
+    TG_CUDA(cudaEventRecord(c->ev[32], st));
+    TG_CUDA(cudaMemcpyAsync(d_pts, pts, n * d * sizeof(float), cudaMemcpyHostToDevice, st));
+    if (span) {
+        unsigned int* flag = next_flag(c);
+        TG_TRY(launch_classify(d_pts, n * d, flag, st, c->sms));
+        // Copy pipeline: pieces of block rows, each piece's D2H overlaps the next kernel.
+        const uint64_t bytes = elems * sizeof(float);
+        uint32_t Q = (s == TG_REC) ? 1 : (uint32_t)std::min<uint64_t>(16, std::max<uint64_t>(1, bytes >> 28));
+        Q = (uint32_t)std::min<uint64_t>(Q, std::max<uint64_t>(1, b1 - b0));
+        // piece bounds: split [b0, b1) by element count
+        std::vector<uint64_t> pr(Q + 1);
+        pr[0] = b0;
+        pr[Q] = b1;
+        for (uint32_t q = 1; q < Q; ++q) {
+            const uint64_t target = tri(b0) + (tri(b1) - tri(b0)) * q / Q;
+            uint64_t r = fix_row(ltm_row_guess(target, kExact, true), target, true);
+            pr[q] = std::min(std::max(r, pr[q - 1]), b1);
+        }
+        const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * span_slots()) / rho);
+        OutWin ow{eb, ee};
+        uint64_t lo = 0;
+        for (uint32_t q = 0; q < Q; ++q) {
+            SpanGeom g;
+            TG_TRY(plan_span(s, n, rho, pr[q], pr[q + 1], C, &g));
+            TG_TRY(launch_span_edm(d, g, ow, d_pts, d_out, flag, st, o.persistent != 0, c->sms));
+            TG_CUDA(cudaEventRecord(c->ev[q], st));
+            const uint64_t piece_end = tri(std::min<uint64_t>(n, pr[q + 1] * rho)) - eb;
+            const uint64_t hi = (q + 1 == Q) ? elems : std::min<uint64_t>(elems, (piece_end + 3) & ~3ull);
+            if (hi > lo) {
+                TG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev[q], 0));
+                TG_CUDA(cudaMemcpyAsync(out + lo, d_out + lo, (hi - lo) * sizeof(float),
+                                        cudaMemcpyDeviceToHost, c->copy_stream));
+                lo = hi;
+            }
+        }
+        TG_CUDA(cudaEventRecord(c->ev[33], st));
+    } else {
+        TG_TRY(launch_grid(plan_grid(s, n, rho), EdmBody{d_pts, d_out, d}, st));
+        TG_CUDA(cudaEventRecord(c->ev[33], st));
+        TG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev[33], 0));
+        TG_CUDA(cudaMemcpyAsync(out, d_out, elems * sizeof(float), cudaMemcpyDeviceToHost, c->copy_stream));
+    }
+    TG_CUDA(cudaStreamSynchronize(c->copy_stream));
+    TG_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    TG_CUDA(cudaEventElapsedTime(&ms, c->ev[32], c->ev[33]));
+    st_local.wall_time_ns = (uint64_t)std::llround((double)ms * 1e6);
+    if (stats) *stats = st_local;
+    return TG_OK;
+}
+
+tg_status tg_coverage_ok(tg_strategy s, uint64_t n, uint32_t rho, int device, int* ok) {
+    g_launches = 0;
+    TG_TRY(validate_problem(s, n, rho));
+    DeviceCtx* c;
+    TG_TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = c->stream;
+    const uint64_t cells = tri(n);
+    TG_TRY(ensure_buf(c->bufs[2], cells * sizeof(uint32_t)));
+    uint32_t* counts = static_cast<uint32_t*>(c->bufs[2].p);
+    TG_CUDA(cudaMemsetAsync(counts, 0, cells * sizeof(uint32_t), st));
+    TG_TRY(launch_grid(plan_grid(s, n, rho), CountBody{counts}, st));
+    unsigned long long init[2] = {0, ~0ull};
+    TG_CUDA(cudaMemcpyAsync(c->scratch + 1, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    const uint64_t blocks = std::min<uint64_t>(ceil_div(cells, 256), (uint64_t)c->sms * 16);
+    check_counts_kernel<<<(unsigned)blocks, 256, 0, st>>>(counts, n, s != TG_UTM, c->scratch + 1, c->scratch + 2);
+    ++g_launches;
+    TG_CUDA(cudaGetLastError());
+    unsigned long long res[2];
+    TG_CUDA(cudaMemcpyAsync(res, c->scratch + 1, sizeof(res), cudaMemcpyDeviceToHost, st));
+    TG_CUDA(cudaStreamSynchronize(st));
+    *ok = res[0] == 0 ? 1 : 0;
+    return TG_OK;
+}
+
+tg_status tg_lambda_sweep(int engine, int with_diag, int fixup, uint64_t begin, uint64_t end,
+                          int device, uint64_t* mismatches, uint64_t* first) {
+    g_launches = 0;
+    if (engine < 0 || engine > 3) return fail(TG_EINVAL, "lambda_sweep: unknown engine");
+    if (end < begin) return fail(TG_EINVAL, "lambda_sweep: end < begin");
+    if (end > (1ull << 40)) return fail(TG_EINVAL, "lambda_sweep: end beyond 2^40");
+    DeviceCtx* c;
+    TG_TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = c->stream;
+    unsigned long long init[2] = {0, ~0ull};
+    TG_CUDA(cudaMemcpyAsync(c->scratch + 1, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    if (end > begin) {
+        const uint64_t blocks = std::min<uint64_t>(ceil_div(end - begin, 256), (uint64_t)c->sms * 32);
+        lambda_sweep_kernel<<<(unsigned)blocks, 256, 0, st>>>(engine, with_diag, fixup, begin, end,
+                                                              c->scratch + 1, c->scratch + 2);
+        ++g_launches;
+        TG_CUDA(cudaGetLastError());
+    }
+    unsigned long long res[2];
+    TG_CUDA(cudaMemcpyAsync(res, c->scratch + 1, sizeof(res), cudaMemcpyDeviceToHost, st));
+    TG_CUDA(cudaStreamSynchronize(st));
+    *mismatches = res[0];
+    *first = res[1];
+    return TG_OK;
+}
+
+tg_status tg_sqrt_selftest(uint32_t lo, uint32_t hi, int device, uint64_t* mismatches) {
+    g_launches = 0;
+    DeviceCtx* c;
+    TG_TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = c->stream;
+    TG_CUDA(cudaMemsetAsync(c->scratch + 1, 0, sizeof(unsigned long long), st));
+    if (hi > lo) {
+        const uint64_t blocks = std::min<uint64_t>(ceil_div((uint64_t)hi - lo, 256), (uint64_t)c->sms * 32);
+        sqrt_selftest_kernel<<<(unsigned)blocks, 256, 0, st>>>(lo, hi, c->scratch + 1);
+        ++g_launches;
+        TG_CUDA(cudaGetLastError());
+    }
+    unsigned long long r;
+    TG_CUDA(cudaMemcpyAsync(&r, c->scratch + 1, sizeof(r), cudaMemcpyDeviceToHost, st));
+    TG_CUDA(cudaStreamSynchronize(st));
+    *mismatches = r;
+    return TG_OK;
+}
+
+tg_status tg_gen_values(uint64_t count, uint64_t seed, float* out, const tg_launch_opts* opts) {
+    g_launches = 0;
+    const tg_launch_opts o = opts ? *opts : default_opts();
+    if (!out) return fail(TG_EINVAL, "gen_values: NULL output");
+    DeviceCtx* c;
+    TG_TRY(get_ctx(o.device, &c));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(o.stream);
+    if (count) {
+        const uint64_t blocks = std::min<uint64_t>(ceil_div(count, 256), (uint64_t)c->sms * 16);
+        gen_points_kernel<<<(unsigned)blocks, 256, 0, st>>>(count, seed, out);
+        ++g_launches;
+        TG_CUDA(cudaGetLastError());
+    }
+    if (!o.async) TG_CUDA(cudaStreamSynchronize(st));
+    return TG_OK;
+}
+
+tg_status tg_gen_points_host(uint64_t n, uint32_t d, uint64_t seed, float* out, int device) {
+    if (n == 0) return fail(TG_EINVAL, "gen_points: N must be >= 1");
+    if (n > kMaxElems) return fail(TG_EINVAL, "gen_points: N exceeds the 2^20 cap");
+    if (d < 1 || d > 4) return fail(TG_EINVAL, "gen_points: d must be in [1, 4]");
+    DeviceCtx* c;
+    TG_TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    TG_TRY(ensure_buf(c->bufs[3], n * d * sizeof(float)));
+    tg_launch_opts o = default_opts();
+    o.device = c->dev;
+    o.stream = c->stream;
+    o.async = 1;
+    TG_TRY(tg_gen_values(n * d, seed, static_cast<float*>(c->bufs[3].p), &o));
+    TG_CUDA(cudaMemcpyAsync(out, c->bufs[3].p, n * d * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    TG_CUDA(cudaStreamSynchronize(c->stream));
+    return TG_OK;
+}
+
+}  // extern "C"
