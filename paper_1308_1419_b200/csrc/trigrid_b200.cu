@@ -254,6 +254,7 @@ bool span_eligible(tg_strategy s, uint32_t rho) {
 tg_status plan_span(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64_t b1, uint32_t C,
                     SpanGeom* g) {
     std::memset(g, 0, sizeof(*g));
+    g->one = 1.0f;
     g->rho = rho;
     g->C = C;
     g->n = n;
@@ -307,14 +308,22 @@ uint64_t span_grid(const SpanGeom& g, bool persistent, int sms, int occ) {
     return std::min<uint64_t>(grid, 0x7fffffffull);
 }
 
-template <int D, int P>
+int span_packed() {
+    static int v = [] {
+        const char* e = std::getenv("TG_SPAN_PACKED");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
+template <int D, int P, bool PK>
 tg_status launch_span_edm_t(const SpanGeom& g, OutWin ow, const float* pts, float* out,
                             const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
     static int occ = -1;
-    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_edm_kernel<D, P>, kWarpsPerCta * 32, 0);
+    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_edm_kernel<D, P, PK>, kWarpsPerCta * 32, 0);
     const uint64_t grid = span_grid(g, persistent, sms, occ);
     if (!grid) return TG_OK;
-    span_edm_kernel<D, P><<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, ow, pts, out, flag);
+    span_edm_kernel<D, P, PK><<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, ow, pts, out, flag);
     ++g_launches;
     TG_CUDA(cudaGetLastError());
     return TG_OK;
@@ -323,12 +332,18 @@ tg_status launch_span_edm_t(const SpanGeom& g, OutWin ow, const float* pts, floa
 template <int P>
 tg_status launch_span_edm_p(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
                             const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
+    const bool pk = span_packed() != 0;
+#define TG_EDM_CASE(DD)                                                                          \
+    case DD:                                                                                     \
+        return pk ? launch_span_edm_t<DD, P, true>(g, ow, pts, out, flag, st, persistent, sms)   \
+                  : launch_span_edm_t<DD, P, false>(g, ow, pts, out, flag, st, persistent, sms);
     switch (d) {
-        case 1: return launch_span_edm_t<1, P>(g, ow, pts, out, flag, st, persistent, sms);
-        case 2: return launch_span_edm_t<2, P>(g, ow, pts, out, flag, st, persistent, sms);
-        case 3: return launch_span_edm_t<3, P>(g, ow, pts, out, flag, st, persistent, sms);
-        case 4: return launch_span_edm_t<4, P>(g, ow, pts, out, flag, st, persistent, sms);
+        TG_EDM_CASE(1)
+        TG_EDM_CASE(2)
+        TG_EDM_CASE(3)
+        TG_EDM_CASE(4)
     }
+#undef TG_EDM_CASE
     return fail(TG_EINVAL, "span EDM supports d in [1, 4]");
 }
 
