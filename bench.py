@@ -318,6 +318,42 @@ def run_ours(args):
                 r["I_write_vs_bb"] = bb["write_ms"] / r["write_ms"]
         per_mapping = rows
 
+    # ---- the other BASELINE.json configs (parity cases; timed for reference)
+    other = {}
+    if not args.quick:
+        # C3: collision table N=32768 (bit-packed no-diagonal table + count)
+        nc, r_max = 32768, 0.0625
+        sph = tg.gen_values(nc * 4, SEED, dev).view(nc, 4)
+        c_ms = time_steps(lambda: tg.collide(sph, r_max, strategy="ltm-r", shard=(rank, world) if world > 1 else None,
+                                             stream=stream, sync=False), 5, 2)
+        _, hits = tg.collide(sph, r_max, strategy="ltm-r", shard=(rank, world) if world > 1 else None)
+        p0, p1 = tg.shard_elems(nc, RHO, rank, world, with_diag=False)
+        other["C3_collide_n32768"] = {"ms": c_ms, "pairs_per_s": tri(nc - 1) / (c_ms / 1e3),
+                                      "hits_shard": int(hits.item()), "r_max": r_max,
+                                      "out_bytes_shard": 4 * ((p1 - p0 + 31) // 32)}
+        # C4: EDM N=65536, d=64, direct (bit-exact) wide span kernel
+        if True:
+            p64 = tg.gen_values(n * 64, SEED, dev).view(n, 64)
+            w_ms = time_steps(lambda: tg.launch("edm", strategy, n, points=p64, out=out, d=64, rho=RHO,
+                                                shard=shard, stream=stream, sync=False), 3, 1)
+            other["C4_edm_n65536_d64_direct"] = {"ms": w_ms, "elems_per_s": tri(n) / (w_ms / 1e3),
+                                                 "fp32_ops_per_cell": 3 * 64}
+            del p64
+        # C5: EDM N=131072, d=3 -- this rank's lambda shard of the 34.4 GB output
+        n5 = 131072
+        b5, e5 = tg.shard_elems(n5, RHO, rank, world)
+        if 4 * (e5 - b5) < 40e9:
+            p5 = tg.gen_values(n5 * 3, SEED, dev).view(n5, 3)
+            o5 = torch.empty(e5 - b5, dtype=torch.float32, device=dev)
+            f_ms = time_steps(lambda: tg.launch("edm", strategy, n5, points=p5, out=o5, d=3, rho=RHO,
+                                                shard=(rank, world) if world > 1 else None, stream=stream,
+                                                sync=False), 3, 1)
+            other["C5_edm_n131072_d3"] = {"ms": f_ms, "elems_per_s_total": tri(n5) / (f_ms / 1e3),
+                                          "shard_gb": 4 * (e5 - b5) / 1e9,
+                                          "hbm_gbs_per_gpu": 4 * (e5 - b5) / (f_ms / 1e3) / 1e9}
+            del p5, o5
+        torch.cuda.empty_cache()
+
     # ---- e2e through the public drop-in with pinned host buffers
     host_pts = torch.from_numpy(pts.cpu().numpy()).pin_memory().numpy()
     host_out = torch.empty(cells_local, dtype=torch.float32).pin_memory().numpy()
@@ -356,6 +392,7 @@ def run_ours(args):
         "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
         "gpu_launches": launches_per_step * args.steps,
         "per_mapping": per_mapping,
+        "other_configs": other,
         "verify": {"row": check_row},
     }
     if rank == 0:

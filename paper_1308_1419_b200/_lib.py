@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtrigrid_b200.so")
+# TG_LIB_PATH: an alternative in-tree build of the same library (A/B tuning only)
+LIB_PATH = os.environ.get("TG_LIB_PATH") or os.path.join(HERE, "libtrigrid_b200.so")
 
 TG_OK, TG_EINVAL, TG_ERANGE, TG_ERUNTIME, TG_ECUDA, TG_ENOMEM = range(6)
 STRATEGIES = {"bb": 0, "ltm-x": 1, "ltm-n": 2, "ltm-r": 3, "ltm-exact": 4, "utm": 5, "rb": 6, "rec": 7}

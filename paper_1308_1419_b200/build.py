@@ -44,22 +44,33 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: tuple = ()) -> str:
+    """Build the library; `variant` + `defines` build an A/B copy
+    (libtrigrid_b200_<variant>.so) used only through TG_LIB_PATH."""
+    lib = LIB if variant is None else os.path.join(HERE, f"libtrigrid_b200_{variant}.so")
+    if not force and variant is None and up_to_date():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *SOURCES]
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+           "-o", lib + ".tmp", *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libtrigrid_b200.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
-        f.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    if variant is None:
+        with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
+            f.write(res.stderr)
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--variant" in sys.argv:
+        k = sys.argv.index("--variant")
+        name, defs = sys.argv[k + 1], tuple(sys.argv[k + 2:])
+        print(build(force=True, variant=name, defines=defs))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -184,8 +185,9 @@ struct Buf {
 };
 
 struct DeviceCtx {
-    std::mutex mu;
-    bool init = false;
+    std::mutex mu;       // guards the cached buffers / internal streams of the host drop-ins
+    std::mutex init_mu;  // one-time initialisation
+    std::atomic<bool> init{false};
     int dev = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;       // internal compute stream (host drop-ins)
@@ -220,8 +222,12 @@ tg_status get_ctx(int device, DeviceCtx** out) {
     if (dev >= 64) return fail(TG_EINVAL, "device ordinal out of range");
     TG_CUDA(cudaSetDevice(dev));
     DeviceCtx& c = g_ctx[dev];
-    std::lock_guard<std::mutex> lk(c.mu);
-    if (!c.init) {
+    if (c.init.load(std::memory_order_acquire)) {
+        *out = &c;
+        return TG_OK;
+    }
+    std::lock_guard<std::mutex> lk(c.init_mu);  // not c.mu: callers may hold c.mu
+    if (!c.init.load(std::memory_order_relaxed)) {
         c.dev = dev;
         TG_CUDA(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
         TG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
@@ -229,7 +235,7 @@ tg_status get_ctx(int device, DeviceCtx** out) {
         TG_CUDA(cudaMalloc(&c.flags, kFlagRing * sizeof(unsigned int)));
         TG_CUDA(cudaMalloc(&c.scratch, 256));
         for (auto& e : c.ev) TG_CUDA(cudaEventCreate(&e));
-        c.init = true;
+        c.init.store(true, std::memory_order_release);
     }
     *out = &c;
     return TG_OK;
@@ -351,6 +357,23 @@ tg_status launch_span_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float*
                           const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
     return span_slots() == 2 ? launch_span_edm_p<2>(d, g, ow, pts, out, flag, st, persistent, sms)
                              : launch_span_edm_p<1>(d, g, ow, pts, out, flag, st, persistent, sms);
+}
+
+// d > 4: CTA-per-run tiled kernel (rho == 16, runs of <= 128 columns).
+tg_status launch_wide_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
+                          const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
+    if (g.rho != 16 || g.C != 8) return fail(TG_EINVAL, "wide EDM span kernel needs rho == 16");
+    uint64_t grid = std::min<uint64_t>(g.units, 0x7fffffffull);
+    if (persistent) {
+        static int occ = -1;
+        if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide_edm_kernel, 256, 0);
+        grid = std::min<uint64_t>(grid, (uint64_t)sms * std::max(occ, 1));
+    }
+    if (!grid) return TG_OK;
+    wide_edm_kernel<<<(unsigned)grid, 256, 0, st>>>(g, ow, pts, d, out, flag);
+    ++g_launches;
+    TG_CUDA(cudaGetLastError());
+    return TG_OK;
 }
 
 tg_status launch_classify(const float* pts, uint64_t count, unsigned int* flag, cudaStream_t st, int sms) {
@@ -680,7 +703,7 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
     DeviceCtx* c;
     TG_TRY(get_ctx(o.device, &c));
     cudaStream_t st = reinterpret_cast<cudaStream_t>(o.stream);
-    const bool body_span = (kernel == TG_KERNEL_EDM && d <= 4) || kernel == TG_KERNEL_WRITE;
+    const bool body_span = (kernel == TG_KERNEL_EDM && (d <= 4 || rho == 16)) || kernel == TG_KERNEL_WRITE;
     const bool span = resolve_span(o, s, rho, body_span);
     if (span && !(body_span && span_eligible(s, rho)))
         return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec, rho % 4 == 0 and an edm (d<=4) or write body");
@@ -692,13 +715,18 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
         const auto rows = shard_rows(nb, G);
         const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
         SpanGeom g;
-        const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * span_slots()) / rho);
+        const bool wide = kernel == TG_KERNEL_EDM && d > 4;
+        const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * (wide ? 1 : span_slots())) / rho);
         TG_TRY(plan_span(s, n, rho, b0, b1, C, &g));
         OutWin ow{tri(std::min<uint64_t>(n, b0 * rho)), tri(std::min<uint64_t>(n, b1 * rho))};
         if (kernel == TG_KERNEL_EDM) {
             unsigned int* flag = next_flag(c);
             TG_TRY(launch_classify(pts, n * d, flag, st, c->sms));
-            TG_TRY(launch_span_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms));
+            if (d <= 4) {
+                TG_TRY(launch_span_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms));
+            } else {
+                TG_TRY(launch_wide_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms));
+            }
         } else {
             TG_TRY(launch_span_write(g, ow, static_cast<uint32_t*>(out), st, o.persistent != 0, c->sms));
         }

@@ -23,7 +23,7 @@ def shim_bin(tg):
 
 
 def test_shim_host(shim_bin):
-    r = subprocess.run([shim_bin, "host"], capture_output=True, text=True)
+    r = subprocess.run([shim_bin, "host"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "host checks ok" in r.stdout
 
@@ -31,7 +31,7 @@ def test_shim_host(shim_bin):
 @pytest.mark.gpu
 def test_shim_launch_edm(shim_bin, orc, tmp_path):
     out = tmp_path / "edm.bin"
-    r = subprocess.run([shim_bin, "edm", "2048", "3", str(out)], capture_output=True, text=True)
+    r = subprocess.run([shim_bin, "edm", "2048", "3", str(out)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     got = np.fromfile(out, dtype=np.float32)
     want = orc.edm_reference(orc.gen_points(2048, 3, 42))
