@@ -212,4 +212,28 @@ void ref_edm_session_destroy(ref_edm_session* s) { delete s; }
 
 unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
 
+// CSV: the reference parses `in` (bench.cpp:194-223) and re-emits it
+// (bench.cpp:146-164) to `out` -- pins the GPU harness's CSV bytes.
+int ref_csv_roundtrip(const char* in, const char* out) {
+    return guarded([&] { emit_csv(parse_csv(in), out); });
+}
+
+// PEDM I/O (edm.cpp:65-96).
+int ref_save_pedm(const float* vals, std::uint64_t n, std::uint32_t d, const char* path) {
+    return guarded([&] {
+        PackedEdm e{n, std::vector<float>(vals, vals + tri_count(n, true))};
+        save_packed_edm(e, d, path);
+    });
+}
+
+int ref_load_pedm(const char* path, float* out, std::uint64_t cap, std::uint64_t* n, std::uint32_t* d) {
+    return guarded([&] {
+        const PedmFile f = load_packed_edm(path);
+        *n = f.edm.count;
+        *d = f.features;
+        if (f.edm.values.size() > cap) throw std::out_of_range("buffer too small");
+        std::memcpy(out, f.edm.values.data(), f.edm.values.size() * sizeof(float));
+    });
+}
+
 }  // extern "C"
