@@ -478,6 +478,15 @@ tg_status launch_grid(const std::vector<GridGeom>& passes, Body body, cudaStream
     return TG_OK;
 }
 
+template <class T>
+tg_status launch_diag_fill(T* out, uint64_t n, bool write_table, cudaStream_t st, int sms) {
+    const uint64_t blocks = std::min<uint64_t>(ceil_div(n, 256), (uint64_t)sms * 4);
+    diag_fill_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(out, n, write_table ? 1 : 0);
+    ++g_launches;
+    TG_CUDA(cudaGetLastError());
+    return TG_OK;
+}
+
 // ------------------------------------------------------------- timing
 
 struct Timer {
@@ -688,6 +697,14 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
     const uint32_t G = o.shard_count == 0 ? 1 : o.shard_count;
     tg_dispatch_stats st_local;
     TG_TRY(stats_for(s, n, rho, o.shard_index, G, &st_local));
+    if (G > 1 && (kernel == TG_KERNEL_EDM || kernel == TG_KERNEL_WRITE)) {
+        uint64_t eb, ee;
+        TG_TRY(tg_shard_elems(n, rho, o.shard_index, G, 1, &eb, &ee));
+        if (ee == eb) {  // empty shard (more shards than block rows): nothing to do
+            if (stats) *stats = st_local;
+            return TG_OK;
+        }
+    }
     if (kernel == TG_KERNEL_EDM) {
         if (d < 1) return fail(TG_EINVAL, "launch_edm: features must be >= 1");
         if (!pts || !out) return fail(TG_EINVAL, "launch: EDM kernel needs points and an output buffer");
@@ -735,9 +752,11 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
         switch (kernel) {
             case TG_KERNEL_EDM:
                 TG_TRY(launch_grid(passes, EdmBody{pts, static_cast<float*>(out), d}, st));
+                if (s == TG_UTM) TG_TRY(launch_diag_fill(static_cast<float*>(out), n, false, st, c->sms));
                 break;
             case TG_KERNEL_WRITE:
                 TG_TRY(launch_grid(passes, WriteBody{static_cast<uint32_t*>(out)}, st));
+                if (s == TG_UTM) TG_TRY(launch_diag_fill(static_cast<uint32_t*>(out), n, true, st, c->sms));
                 break;
             case TG_KERNEL_COUNT:
                 TG_TRY(launch_grid(passes, CountBody{static_cast<uint32_t*>(out)}, st));
@@ -871,6 +890,7 @@ tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint
         TG_CUDA(cudaEventRecord(c->ev[33], st));
     } else {
         TG_TRY(launch_grid(plan_grid(s, n, rho), EdmBody{d_pts, d_out, d}, st));
+        if (s == TG_UTM) TG_TRY(launch_diag_fill(d_out, n, false, st, c->sms));
         TG_CUDA(cudaEventRecord(c->ev[33], st));
         TG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev[33], 0));
         TG_CUDA(cudaMemcpyAsync(out, d_out, elems * sizeof(float), cudaMemcpyDeviceToHost, c->copy_stream));
