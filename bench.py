@@ -198,11 +198,18 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # NCCL for the (tiny) timing collectives; TG_DIST_BACKEND=gloo lets the
+    # multi-rank path be exercised with several ranks on one GPU.
+    backend = os.environ.get("TG_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    cdev = dev if backend == "nccl" else torch.device("cpu")
 
     def barrier():
         if world > 1:
@@ -211,7 +218,7 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -280,6 +287,11 @@ def run_ours(args):
                 "kernel": "tg::span_edm_kernel<3,1> (+ classify_points_kernel)",
                 "algorithmic_bytes_per_launch": alg_bytes, "launch_ms_median": k_ms,
                 "peak_source": pk["source"] + " copy bandwidth, burst"}
+
+    # ---- store-only reference: cudaMemset of the same packed buffer
+    fill_ms = time_steps(lambda: out.view(torch.int32).fill_(0), 5, 2)
+    roofline["store_only_peak_gbs"] = 4 * cells_local / (fill_ms / 1e3) / 1e9
+    roofline["frac_of_store_peak"] = achieved / roofline["store_only_peak_gbs"]
 
     # ---- per mapping (I = t_BB / t_strategy, bench.cpp:124-133)
     per_mapping = {}

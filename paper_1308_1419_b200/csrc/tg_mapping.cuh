@@ -134,7 +134,14 @@ TG_HD float engine_sqrt(int engine, float xf) {
         case kNewton: return fmul(xf, fast_inv_sqrt(xf, 3));
         default:
 #if defined(__CUDA_ARCH__)
-            return fmul(xf, rsqrtf(xf));
+        {
+            // MUFU.RSQ directly: every argument here is >= 0.25 (g(lambda))
+            // or >= 1 (utm discriminant), so rsqrtf's denormal rescaling is
+            // dead code and this is bit-identical to rsqrtf.
+            float y;
+            asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(xf));
+            return fmul(xf, y);
+        }
 #else
             return fmul(xf, 1.0f / std::sqrt(xf));
 #endif
