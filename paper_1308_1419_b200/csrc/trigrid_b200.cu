@@ -47,6 +47,7 @@ tg_status fail(tg_status s, const std::string& msg) {
     } while (0)
 
 uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+int span_upw();  // consecutive span units per warp (TG_SPAN_UPW, default 4)
 
 bool is_ltm(tg_strategy s) { return s >= TG_LTM_X && s <= TG_LTM_EXACT; }
 int ltm_engine(tg_strategy s) {
