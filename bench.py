@@ -290,6 +290,7 @@ def run_ours(args):
 
     # ---- store-only reference: cudaMemset of the same packed buffer
     fill_ms = time_steps(lambda: out.view(torch.int32).fill_(0), 5, 2)
+    roofline["write_kernel_ms"] = time_steps(lambda: step(kernel="write", o=out.view(torch.int32)), 5, 2)
     roofline["store_only_peak_gbs"] = 4 * cells_local / (fill_ms / 1e3) / 1e9
     roofline["frac_of_store_peak"] = achieved / roofline["store_only_peak_gbs"]
 
