@@ -47,7 +47,6 @@ tg_status fail(tg_status s, const std::string& msg) {
     } while (0)
 
 uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
-int span_upw();  // consecutive span units per warp (TG_SPAN_UPW, default 4)
 
 bool is_ltm(tg_strategy s) { return s >= TG_LTM_X && s <= TG_LTM_EXACT; }
 int ltm_engine(tg_strategy s) {
@@ -262,7 +261,6 @@ tg_status plan_span(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64
                     SpanGeom* g) {
     std::memset(g, 0, sizeof(*g));
     g->one = 1.0f;
-    g->upw = (uint32_t)span_upw();
     g->rho = rho;
     g->C = C;
     g->n = n;
@@ -308,17 +306,8 @@ tg_status plan_span(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64
     return TG_OK;
 }
 
-int span_upw() {
-    static int v = [] {
-        const char* e = std::getenv("TG_SPAN_UPW");
-        const int x = e ? std::atoi(e) : 4;
-        return x < 1 ? 1 : x;
-    }();
-    return v;
-}
-
 uint64_t span_grid(const SpanGeom& g, bool persistent, int sms, int occ) {
-    const uint64_t need = ceil_div(ceil_div(g.units, g.upw), kWarpsPerCta);
+    const uint64_t need = ceil_div(g.units, kWarpsPerCta);
     if (need == 0) return 0;
     uint64_t grid = need;
     if (persistent) grid = std::min<uint64_t>(need, (uint64_t)sms * std::max(occ, 1));
