@@ -398,10 +398,20 @@ tg_status launch_span_write_p(const SpanGeom& g, OutWin ow, uint32_t* out, cudaS
     return TG_OK;
 }
 
+// Chunk slots per lane of the write kernel: 2 (1 KB contiguous per warp and
+// row) measured 1.27 ms vs 1.50 ms for 1 slot at N=65536 (profiles/r1d_*).
+int write_slots() {
+    static int v = [] {
+        const char* e = std::getenv("TG_WRITE_SLOTS");
+        return (e && std::atoi(e) == 1) ? 1 : 2;
+    }();
+    return v;
+}
+
 tg_status launch_span_write(const SpanGeom& g, OutWin ow, uint32_t* out, cudaStream_t st,
                             bool persistent, int sms) {
-    return span_slots() == 2 ? launch_span_write_p<2>(g, ow, out, st, persistent, sms)
-                             : launch_span_write_p<1>(g, ow, out, st, persistent, sms);
+    return write_slots() == 2 ? launch_span_write_p<2>(g, ow, out, st, persistent, sms)
+                              : launch_span_write_p<1>(g, ow, out, st, persistent, sms);
 }
 
 // --------------------------------------------------------- grid planning
@@ -733,7 +743,8 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
         const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
         SpanGeom g;
         const bool wide = kernel == TG_KERNEL_EDM && d > 4;
-        const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * (wide ? 1 : span_slots())) / rho);
+        const int slots = wide ? 1 : (kernel == TG_KERNEL_WRITE ? write_slots() : span_slots());
+        const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * slots) / rho);
         TG_TRY(plan_span(s, n, rho, b0, b1, C, &g));
         OutWin ow{tri(std::min<uint64_t>(n, b0 * rho)), tri(std::min<uint64_t>(n, b1 * rho))};
         if (kernel == TG_KERNEL_EDM) {
