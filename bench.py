@@ -350,7 +350,17 @@ def run_ours(args):
             w_ms = time_steps(lambda: tg.launch("edm", strategy, n, points=p64, out=out, d=64, rho=RHO,
                                                 shard=shard, stream=stream, sync=False), 3, 1)
             other["C4_edm_n65536_d64_direct"] = {"ms": w_ms, "elems_per_s": tri(n) / (w_ms / 1e3),
-                                                 "fp32_ops_per_cell": 3 * 64}
+                                                 "fp32_ops_per_cell": 3 * 64, "bit_exact": True}
+            try:
+                gm_ms = time_steps(lambda: tg.launch("edm", strategy, n, points=p64, out=out, d=64, rho=RHO,
+                                                     shard=shard, mode="gram", stream=stream, sync=False), 3, 1)
+                other["C4_edm_n65536_d64_gram_tcgen05"] = {
+                    "ms": gm_ms, "elems_per_s": tri(n) / (gm_ms / 1e3),
+                    "hbm_gbs": 4 * cells_local / (gm_ms / 1e3) / 1e9,
+                    "tensor_tflops": 3 * 2 * 64 * 128 * 128 * ((n // 128) * (n // 128 + 1) // 2) / (gm_ms / 1e3) / 1e12,
+                    "bit_exact": False, "tolerance": "|d^2 - d_exact^2| <= 2^-17 (|x_i|^2 + |x_j|^2)"}
+            except RuntimeError as exc:
+                other["C4_edm_n65536_d64_gram_tcgen05"] = {"error": str(exc)}
             del p64
         # C5: EDM N=131072, d=3 -- this rank's lambda shard of the 34.4 GB output
         n5 = 131072

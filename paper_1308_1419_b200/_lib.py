@@ -17,7 +17,7 @@ TG_OK, TG_EINVAL, TG_ERANGE, TG_ERUNTIME, TG_ECUDA, TG_ENOMEM = range(6)
 STRATEGIES = {"bb": 0, "ltm-x": 1, "ltm-n": 2, "ltm-r": 3, "ltm-exact": 4, "utm": 5, "rb": 6, "rec": 7}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 KERNELS = {"dummy": 0, "write": 1, "edm": 2, "count": 3}
-MODES = {"auto": 0, "grid": 1, "span": 2}
+MODES = {"auto": 0, "grid": 1, "span": 2, "gram": 3}
 
 
 class tg_dispatch_stats(C.Structure):

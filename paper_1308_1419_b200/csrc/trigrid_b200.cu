@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/trigrid_b200.h"
+#include "tg_gram.cuh"
 #include "tg_kernels.cuh"
 
 using namespace tg;
@@ -195,7 +196,7 @@ struct DeviceCtx {
     unsigned int* flags = nullptr;       // classify verdicts (ring, one per launch)
     unsigned flag_next = 0;
     unsigned long long* scratch = nullptr;  // [0] sink [1] bad [2] first [3] hits
-    Buf bufs[4];
+    Buf bufs[5];  // [0] pts [1] out (host drop-ins) [2] counts [3] gen [4] gram norms
     cudaEvent_t ev[34];
 };
 
@@ -371,6 +372,41 @@ tg_status launch_wide_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float*
     }
     if (!grid) return TG_OK;
     wide_edm_kernel<<<(unsigned)grid, 256, 0, st>>>(g, ow, pts, d, out, flag);
+    ++g_launches;
+    TG_CUDA(cudaGetLastError());
+    return TG_OK;
+}
+
+// Gram-trick EDM on tcgen05 (tg_gram.cuh) over the block rows [b0, b1) of
+// the rho-block triangle: 128-row tiles covering those rows, tile lambda
+// range [T(ty0), T(ty1)), rows and elements clipped to the window.
+tg_status launch_gram_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, uint64_t b1, OutWin ow,
+                          const float* pts, float* out, float* norms, cudaStream_t st, int sms) {
+    static bool attr = false;
+    if (!attr) {
+        TG_CUDA(cudaFuncSetAttribute(gram_edm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmemBytes));
+        attr = true;
+    }
+    const uint64_t r0 = std::min<uint64_t>(n, b0 * rho), r1 = std::min<uint64_t>(n, b1 * rho);
+    if (r1 <= r0) return TG_OK;
+    GramGeom g{};
+    g.n = n;
+    g.d = d;
+    g.nt = (uint32_t)ceil_div(n, kGT);
+    const uint64_t ty0 = r0 / kGT, ty1 = ceil_div(r1, kGT);
+    g.t0 = tri(ty0);
+    g.t1 = tri(ty1);
+    g.r0 = r0;
+    g.r1 = r1;
+    g.e_base = ow.e_base;
+    g.e_end = ow.e_end;
+    const uint64_t tiles = g.t1 - g.t0;
+    const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)sms);
+    g.per_cta = ceil_div(tiles, grid);
+    const uint64_t nb = std::min<uint64_t>(ceil_div(n, 256), (uint64_t)sms * 8);
+    gram_norms_kernel<<<(unsigned)nb, 256, 0, st>>>(pts, n, d, norms);
+    ++g_launches;
+    gram_edm_kernel<<<(unsigned)ceil_div(tiles, g.per_cta), kGThreads, kGSmemBytes, st>>>(g, pts, norms, out);
     ++g_launches;
     TG_CUDA(cudaGetLastError());
     return TG_OK;
@@ -730,6 +766,22 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
     DeviceCtx* c;
     TG_TRY(get_ctx(o.device, &c));
     cudaStream_t st = reinterpret_cast<cudaStream_t>(o.stream);
+    if (o.mode == TG_MODE_GRAM) {
+        if (kernel != TG_KERNEL_EDM) return fail(TG_EINVAL, "gram mode computes the EDM only");
+        if (!(is_ltm(s) || s == TG_BB))
+            return fail(TG_EINVAL, "gram mode tiles the triangle by g(lambda) (bb / ltm-* strategies)");
+        const uint64_t nb = ceil_div(n, rho);
+        const auto rows = shard_rows(nb, G);
+        const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
+        OutWin ow{tri(std::min<uint64_t>(n, b0 * rho)), tri(std::min<uint64_t>(n, b1 * rho))};
+        TG_TRY(ensure_buf(c->bufs[4], n * sizeof(float)));
+        Timer timer(st, !o.async);
+        TG_TRY(launch_gram_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out),
+                               static_cast<float*>(c->bufs[4].p), st, c->sms));
+        TG_TRY(timer.finish(&st_local));
+        if (stats) *stats = st_local;
+        return TG_OK;
+    }
     const bool body_span = (kernel == TG_KERNEL_EDM && (d <= 4 || rho == 16)) || kernel == TG_KERNEL_WRITE;
     const bool span = resolve_span(o, s, rho, body_span);
     if (span && !(body_span && span_eligible(s, rho)))

@@ -1,0 +1,57 @@
+"""Gram-trick EDM on tcgen05 (mode="gram"): NOT bit-exact by design.  Stated
+tolerance (tg_gram.cuh):
+    |d_gram^2 - d_exact^2| <= 2^-17 * (|x_i|^2 + |x_j|^2),   d_gram(i, i) == 0
+checked against the exact oracle on every packed cell."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TOL = 2.0 ** -17
+
+
+def _gram(tg, cuda, pts_np, shard=None, strategy="ltm-r"):
+    import torch
+    pts = torch.from_numpy(pts_np).to(cuda)
+    return tg.edm(pts, strategy=strategy, mode="gram", shard=shard).cpu().numpy()
+
+
+def _check(orc, pts, got):
+    n = pts.shape[0]
+    want = orc.edm_reference(pts).astype(np.float64)
+    i = np.repeat(np.arange(n), np.arange(1, n + 1))
+    j = np.arange(want.size) - np.repeat(np.arange(n) * (np.arange(n) + 1) // 2, np.arange(1, n + 1))
+    nrm = (pts.astype(np.float64) ** 2).sum(1)
+    err = np.abs(got.astype(np.float64) ** 2 - want ** 2)
+    bound = TOL * (nrm[i] + nrm[j])
+    assert np.all(got[i == j] == 0.0)
+    worst = float(np.max(err / np.maximum(bound, 1e-30)))
+    assert np.all(err <= bound), f"max err/bound = {worst}"
+    return worst
+
+
+@pytest.mark.parametrize("n,d", [(1, 8), (100, 8), (128, 64), (200, 64), (1000, 64), (777, 100), (4096, 64), (300, 3)])
+def test_gram_tolerance(tg, orc, cuda, n, d):
+    pts = orc.gen_points(n, d, 11 + d)
+    _check(orc, pts, _gram(tg, cuda, pts))
+
+
+def test_gram_shards_and_bb(tg, orc, cuda):
+    pts = orc.gen_points(1500, 64, 5)
+    whole = _gram(tg, cuda, pts)
+    parts = [_gram(tg, cuda, pts, shard=(g, 4)) for g in range(4)]
+    assert np.concatenate(parts).tobytes() == whole.tobytes()
+    assert _gram(tg, cuda, pts, strategy="bb").tobytes() == whole.tobytes()
+
+
+def test_gram_c4_full_size_sampled(tg, orc, cuda):
+    import torch
+    n, d = 65536, 64
+    pts_np = orc.gen_points(n, d, 42)
+    out = tg.edm(torch.from_numpy(pts_np).to(cuda), strategy="ltm-r", mode="gram")
+    rng = np.random.default_rng(3)
+    nrm = (pts_np.astype(np.float64) ** 2).sum(1)
+    for r in [0, 127, 128, 4095, 65535] + [int(x) for x in rng.integers(0, n, 12)]:
+        got = out[r * (r + 1) // 2: (r + 1) * (r + 2) // 2].cpu().numpy().astype(np.float64)
+        want = orc.edm_rows(pts_np, r, r + 1).astype(np.float64)
+        assert got[r] == 0.0
+        assert np.all(np.abs(got ** 2 - want ** 2) <= TOL * (nrm[r] + nrm[: r + 1])), r
