@@ -112,11 +112,20 @@ __device__ __forceinline__ void gram_stage(const float* __restrict__ pts, uint64
     for (uint32_t v = threadIdx.x; v < kGT * (kGK / 4); v += kGThreads) {
         const uint32_t m = v / (kGK / 4), kq = v % (kGK / 4);
         const uint64_t row = row0 + m;
+        const uint32_t kb = k0 + 4 * kq;
         float a[4];
+        if (row < n && (d & 3) == 0 && kb + 4 <= d) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(pts + row * d + kb));
+            a[0] = t.x;
+            a[1] = t.y;
+            a[2] = t.z;
+            a[3] = t.w;
+        } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t k = k0 + 4 * kq + q;
-            a[q] = (row < n && k < d) ? __ldg(pts + row * d + k) : 0.0f;
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t k = kb + q;
+                a[q] = (row < n && k < d) ? __ldg(pts + row * d + k) : 0.0f;
+            }
         }
         const uint32_t off = umma_off(m, 4 * kq);
         *reinterpret_cast<float4*>(s_hi + off) =

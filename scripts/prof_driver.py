@@ -1,0 +1,42 @@
+"""Run one td-kernel configuration a few times (for ncu -k regex:... captures).
+
+    python scripts/prof_driver.py edm   --n 65536 --d 3  --strategy ltm-r [--mode span|grid|gram]
+    python scripts/prof_driver.py write --n 65536 --strategy ltm-r
+    python scripts/prof_driver.py collide --n 32768
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("kernel", choices=["edm", "write", "collide"])
+    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--d", type=int, default=3)
+    ap.add_argument("--strategy", default="ltm-r")
+    ap.add_argument("--mode", default="auto")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    import torch
+
+    from paper_1308_1419_b200 import trigrid as tg
+    n = a.n
+    if a.kernel == "collide":
+        sph = tg.gen_values(n * 4, 42).view(n, 4)
+        for _ in range(a.reps):
+            tg.collide(sph, 0.0625, strategy=a.strategy, mode=a.mode)
+    else:
+        out = torch.empty(n * (n + 1) // 2, dtype=torch.float32 if a.kernel == "edm" else torch.int32, device="cuda")
+        pts = tg.gen_values(n * a.d, 42).view(n, a.d) if a.kernel == "edm" else None
+        for _ in range(a.reps):
+            tg.launch(a.kernel, a.strategy, n, points=pts, out=out, d=a.d if pts is not None else 0, mode=a.mode)
+    torch.cuda.synchronize()
+    print("done")
+
+
+if __name__ == "__main__":
+    main()
