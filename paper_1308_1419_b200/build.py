@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtrigrid_b200.so")
 SOURCES = [os.path.join(CSRC, "trigrid_b200.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("tg_kernels.cuh", "tg_mapping.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("tg_kernels.cuh", "tg_mapping.cuh", "tg_gram.cuh")] + [
     os.path.join(ROOT, "include", "trigrid_b200.h")]
 
 NVCC_FLAGS = [

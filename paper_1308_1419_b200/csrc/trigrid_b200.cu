@@ -196,7 +196,7 @@ struct DeviceCtx {
     unsigned int* flags = nullptr;       // classify verdicts (ring, one per launch)
     unsigned flag_next = 0;
     unsigned long long* scratch = nullptr;  // [0] sink [1] bad [2] first [3] hits
-    Buf bufs[5];  // [0] pts [1] out (host drop-ins) [2] counts [3] gen [4] gram norms
+    Buf bufs[6];  // [0] pts [1] out (host drop-ins) [2] counts [3] gen [4] gram norms [5] gram operands
     cudaEvent_t ev[34];
 };
 
@@ -410,6 +410,63 @@ tg_status launch_gram_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, uin
     ++g_launches;
     gram_edm_kernel<<<(unsigned)ceil_div(tiles, g.per_cta), kGThreads, kGSmemBytes, st>>>(g, pts, norms, out);
     ++g_launches;
+    TG_CUDA(cudaGetLastError());
+    return TG_OK;
+}
+
+// A/B switch: TG_GRAM_V1=1 forces the first (unpipelined 3xTF32) Gram kernel.
+bool gram_v1() {
+    static bool v = [] {
+        const char* e = std::getenv("TG_GRAM_V1");
+        return e && std::atoi(e) != 0;
+    }();
+    return v;
+}
+
+// Pipelined fp16-split Gram EDM (tg_gram.cuh v2) for d <= 128: prep (norms,
+// max |x|) -> split (hi/lo operands in UMMA layout) -> warp-specialised kernel.
+tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, uint64_t b1, OutWin ow,
+                           const float* pts, float* out, DeviceCtx* c, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        TG_CUDA(cudaFuncSetAttribute(gram2_edm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+        attr = true;
+    }
+    const uint64_t r0 = std::min<uint64_t>(n, b0 * rho), r1 = std::min<uint64_t>(n, b1 * rho);
+    if (r1 <= r0) return TG_OK;
+    const uint32_t nk = (uint32_t)ceil_div(d, 64);
+    const uint64_t nt = ceil_div(n, kGT), n_pad = nt * kGT;
+    const uint64_t op_bytes = nt * nk * (uint64_t)kG2Slice;
+    TG_TRY(ensure_buf(c->bufs[4], n_pad * sizeof(float)));
+    TG_TRY(ensure_buf(c->bufs[5], 2 * op_bytes + 256));
+    float* norms = static_cast<float*>(c->bufs[4].p);
+    uint8_t* opA = static_cast<uint8_t*>(c->bufs[5].p);
+    uint8_t* opB = opA + op_bytes;
+    unsigned int* maxbits = reinterpret_cast<unsigned int*>(opB + op_bytes);
+    TG_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned int), st));
+    const unsigned pb = (unsigned)std::min<uint64_t>(ceil_div(n_pad, 256), (uint64_t)c->sms * 8);
+    gram_prep_kernel<<<pb, 256, 0, st>>>(pts, n, n_pad, d, norms, maxbits);
+    const unsigned sb = (unsigned)std::min<uint64_t>(ceil_div(n_pad * nk * 8, 256), (uint64_t)c->sms * 16);
+    gram_split_kernel<<<sb, 256, 0, st>>>(pts, n, n_pad, d, nk, maxbits, opA, opB);
+    Gram2Geom g{};
+    g.n = n;
+    g.nk = nk;
+    const uint64_t fixed = 8ull * kG2EpiBytes + 256;
+    g.ring = (uint32_t)std::min<uint64_t>(4, (232448 - fixed - nk * (uint64_t)kG2Slice) / kG2Slice);
+    const uint64_t ty0 = r0 / kGT, ty1 = ceil_div(r1, kGT);
+    g.t0 = tri(ty0);
+    g.t1 = tri(ty1);
+    g.r0 = r0;
+    g.r1 = r1;
+    g.e_base = ow.e_base;
+    g.e_end = ow.e_end;
+    const uint64_t tiles = g.t1 - g.t0;
+    const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)c->sms);
+    g.per_cta = ceil_div(tiles, grid);
+    const size_t smem = (nk + g.ring) * (size_t)kG2Slice + 8 * (size_t)kG2EpiBytes + 8 * (6 + 2 * g.ring) + 16;
+    gram2_edm_kernel<<<(unsigned)ceil_div(tiles, g.per_cta), kG2Threads, smem, st>>>(g, opA, opB, norms, maxbits,
+                                                                                     out);
+    g_launches += 3;
     TG_CUDA(cudaGetLastError());
     return TG_OK;
 }
@@ -776,10 +833,14 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
         const auto rows = shard_rows(nb, G);
         const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
         OutWin ow{tri(std::min<uint64_t>(n, b0 * rho)), tri(std::min<uint64_t>(n, b1 * rho))};
-        TG_TRY(ensure_buf(c->bufs[4], n * sizeof(float)));
         Timer timer(st, !o.async);
-        TG_TRY(launch_gram_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out),
-                               static_cast<float*>(c->bufs[4].p), st, c->sms));
+        if (d <= 64 * kG2MaxNk && !gram_v1()) {
+            TG_TRY(launch_gram2_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out), c, st));
+        } else {
+            TG_TRY(ensure_buf(c->bufs[4], n * sizeof(float)));
+            TG_TRY(launch_gram_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out),
+                                   static_cast<float*>(c->bufs[4].p), st, c->sms));
+        }
         TG_TRY(timer.finish(&st_local));
         if (stats) *stats = st_local;
         return TG_OK;

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--strategy", default="ltm-r")
     ap.add_argument("--mode", default="auto")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--time", action="store_true", help="print the median launch time (CUDA events)")
     a = ap.parse_args()
     import torch
 
@@ -32,8 +33,19 @@ def main():
     else:
         out = torch.empty(n * (n + 1) // 2, dtype=torch.float32 if a.kernel == "edm" else torch.int32, device="cuda")
         pts = tg.gen_values(n * a.d, 42).view(n, a.d) if a.kernel == "edm" else None
+        ts = []
         for _ in range(a.reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             tg.launch(a.kernel, a.strategy, n, points=pts, out=out, d=a.d if pts is not None else 0, mode=a.mode)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        if a.time:
+            ts.sort()
+            ms = ts[len(ts) // 2]
+            print(f"{a.kernel} n={n} d={a.d} {a.strategy} mode={a.mode}: median {ms:.4f} ms "
+                  f"({4 * n * (n + 1) / 2 / ms / 1e6:.1f} GB/s of packed output) over {a.reps}")
     torch.cuda.synchronize()
     print("done")
 
