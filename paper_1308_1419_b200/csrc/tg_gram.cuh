@@ -289,50 +289,67 @@ __global__ void gram_norms_kernel(const float* __restrict__ pts, uint64_t n, uin
 //    (x * 2^s = hi + lo, s a global power of two putting max|x| in
 //    [2^14, 2^15), so hi/lo stay in fp16's normal range and the pair carries
 //    ~22 significant bits) and laid out in global memory in the canonical
-//    K-major no-swizzle UMMA layout, one 32 KB (hi 16 KB | lo 16 KB) block per
-//    (128-row tile, 64-feature slice).  A tile's operand is therefore one
-//    contiguous cp.async.bulk copy (no tensor map, no per-thread staging), and
-//    kind::f16 runs at twice the tf32 rate with half the L2 bytes.
-//  * The A copy (tile rows) is stored ROW-PERMUTED: TMEM lane quarter q holds
-//    the 32 tile rows r with T(r) = q (mod 4).  The packed element T(i) + j of
-//    every row a warp reads from TMEM then has the same 16-byte alignment
-//    shift, so the realignment of a row segment onto aligned float4 chunks is a
-//    warp-uniform compile-time register selection (no divergence).
-//  * Roles: warp 0 = bulk-copy producer (A resident while the tile row stays,
-//    B through a ring of 32 KB stages), warp 1 = MMA issuer (3 x 4
-//    tcgen05.mma M=128 N=128 K=16 per 64-feature slice: hi*hi + hi*lo + lo*hi),
-//    warps 2..9 = epilogue (lane quarter warp % 4, column half).  The fp32
-//    accumulator is double-buffered in TMEM (2 x 128 columns), so the MMAs of
-//    tile t+1 run under the epilogue / HBM stores of tile t.
-//  * Epilogue per warp: 32 rows x 64 columns: tcgen05.ld -> release the TMEM
-//    buffer -> d = sqrt(max(|x_i|^2 + |x_j|^2 - 2 g, 0)) -> realigned chunks
-//    to a per-warp shared buffer (32 rows x 17 chunks, conflict-free) ->
-//    transposed read -> STG.128 of every full 16-byte chunk, lanes on
-//    consecutive chunks of a row (coalesced); scalar stores only for the two
-//    partial chunks at the ends of each 64-column row segment.
-constexpr int kG2Threads = 320;               // 10 warps
-constexpr uint32_t kG2Slice = 32768;          // one (tile, 64-feature slice): hi | lo fp16
+//    K-major no-swizzle UMMA layout, so every operand stage is a contiguous
+//    cp.async.bulk copy (no tensor map, no per-thread staging), and kind::f16
+//    runs at twice the tf32 rate with half the L2 bytes.
+//  * Row tile (MMA A, M = 128 = TMEM lanes) is stored ROW-PERMUTED: TMEM lane
+//    quarter q holds the 32 tile rows r with T(r) = q (mod 4), so all rows a
+//    warp reads from TMEM share one 16-byte alignment shift of their packed
+//    row start T(i) + j.
+//  * Column operand (MMA B) is N = 136 = 128 + 8 points: the tile plus the
+//    first 8 points of the next column tile.  Each row of tile (i, j) then
+//    OWNS the 32 aligned 16-byte chunks that start in its 128 columns (the
+//    last one spills up to 3 columns into tile j + 1), so every store of an
+//    interior tile is a full aligned STG.128 -- no partial chunks, no
+//    scattered edge stores.  Rows of tile (i, 0) add the <= 3 elements before
+//    their first owned chunk; diagonal / clipped tiles mask per element.
+//  * Roles: warp 0 = bulk-copy producer (row tile resident while the tile row
+//    stays, column operands through a ring of stages), warp 1 = MMA issuer (per
+//    64-feature slice 3 x 4 tcgen05.mma M=128 N=136 K=16: hi*lo + lo*hi +
+//    hi*hi), warps 2..17 = epilogue: TMEM lane quarter warp % 4 (32 rows) x 8
+//    of the 32 chunks.  kG2Acc accumulators in TMEM let the MMAs run ahead.
+//  * Epilogue per warp: tcgen05.ld (32 rows x 40 columns) -> release the
+//    accumulator -> d = sqrt(max(|x_i|^2 + |x_j|^2 - 2 g, 0)) on the 32 owned
+//    columns (warp-uniform compile-time selection of the shift) -> 8 chunks
+//    per row to a per-warp shared buffer -> transposed read -> STG.128, each
+//    warp store instruction 4 rows x 128 contiguous bytes.
+constexpr int kG2EpiWarps = 16;
+constexpr int kG2Threads = 32 * (2 + kG2EpiWarps);
+constexpr uint32_t kG2Slice = 32768;          // row-tile block of one 64-feature slice: hi | lo fp16
 constexpr uint32_t kG2Half = 16384;
+constexpr uint32_t kG2Group = 1024;           // 8 points x 64 features fp16
+constexpr uint32_t kG2N = 136;                // MMA N: column tile + 8 points of the next
+constexpr uint32_t kG2BHalf = 17 * kG2Group;  // 17 groups
+constexpr uint32_t kG2Stage = 2 * kG2BHalf;   // column stage: hi | lo
 constexpr uint32_t kG2LBO = 128;              // K-adjacent core matrices
-constexpr uint32_t kG2SBO = 1024;             // M-adjacent 8-row groups (8 core matrices along K)
-constexpr int kG2Chunks = 17;                 // 16-byte chunks per staged 64-column row segment
-constexpr uint32_t kG2EpiBytes = 32 * kG2Chunks * 16;  // per epilogue warp
+constexpr uint32_t kG2SBO = 1024;             // M/N-adjacent 8-row groups (8 core matrices along K)
 constexpr int kG2MaxNk = 2;                   // d <= 128
-// kind::f16 (A, B fp16, K-major), fp32 accumulate, M = 128, N = 128
-constexpr uint32_t kG2Idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(kGT >> 3) << 17) |
+constexpr uint32_t kG2SmemMax = 232448;
+constexpr uint32_t kG2Acc = 3;                // TMEM accumulators
+constexpr uint32_t kG2AccStride = 144;        // TMEM columns per accumulator (>= kG2N)
+constexpr uint32_t kG2TmemCols = 512;
+constexpr int kG2RowChunks = 9;               // staging row stride in 16-byte chunks (8 used, odd: no conflicts)
+constexpr uint32_t kG2EpiBytes = 32 * kG2RowChunks * 16 + 32 * 4;  // per epilogue warp: staging + column norms
+// kind::f16 (A, B fp16, K-major), fp32 accumulate, M = 128, N = 136
+constexpr uint32_t kG2Idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((kG2N >> 3) << 17) |
                               ((uint32_t)(kGT >> 4) << 24);
 
 struct Gram2Geom {
     uint64_t n;
     uint32_t nk;        // 64-feature slices
-    uint32_t ring;      // B stages
+    uint32_t ring;      // column stages
     uint64_t t0, t1;    // tile-lambda range
     uint64_t per_cta;
     uint64_t r0, r1;    // element rows of the output window
     uint64_t e_base, e_end;
+    uint64_t bslice;    // bytes of one slice of the column operand (hi or lo)
 };
 
-// tile row of TMEM lane p (A row permutation); quarter q holds T(r) = q mod 4
+__host__ __device__ __forceinline__ uint32_t g2_smem_bytes(uint32_t nk, uint32_t ring) {
+    return nk * kG2Slice + ring * kG2Stage + kG2EpiWarps * kG2EpiBytes + 8 * (2 + 2 * kG2Acc + 2 * ring) + 16;
+}
+
+// tile row of TMEM lane p (row-tile permutation); quarter q holds T(r) = q mod 4
 __host__ __device__ __forceinline__ uint32_t g2_perm(uint32_t p) {
     // residues rho (r mod 8) with T(rho) mod 4 = q: q0 {0,7} q1 {1,6} q2 {3,4} q3 {2,5}
     const uint32_t q = p >> 5, l = p & 31;
@@ -382,6 +399,38 @@ __device__ __forceinline__ void g2_bulk_load(uint32_t dst, const void* src, uint
         : "memory");
 }
 
+// next tile of the g(lambda) order: (i, j) -> (i, j + 1), row end -> (i + 1, 0)
+__device__ __forceinline__ void g2_next(Coord& c) {
+    if (c.j == c.i) {
+        ++c.i;
+        c.j = 0;
+    } else {
+        ++c.j;
+    }
+}
+
+// mbarrier wait with a suspend-time hint: a waiting warp sleeps instead of
+// spinning on the issue slots the epilogue warps need
+__device__ __forceinline__ void g2_wait_sleep(uint32_t bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n\t"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
+        "@!done bra WAITS_%=;\n\t}\n" ::"r"(bar),
+        "r"(phase), "r"(0x100000));
+}
+
+__device__ __forceinline__ void g2_ld32(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+
 // Pass 1: |x_i|^2 (fp32 sequential fma, 0 for padding rows) and max |x|.
 __global__ void gram_prep_kernel(const float* __restrict__ pts, uint64_t n, uint64_t n_pad, uint32_t d,
                                  float* __restrict__ norms, unsigned int* __restrict__ maxbits) {
@@ -410,15 +459,18 @@ __device__ __forceinline__ int g2_scale_exp(unsigned int maxbits) {
     return max(-63, min(63, 14 - e));
 }
 
-// Pass 2: x * 2^s = hi + lo in fp16, written to opA (row-permuted) and opB
-// (natural) in the UMMA layout: block (tile t, slice k) at ((t * nk + k) * 32 KB),
-// hi at +0, lo at +16 KB.  One thread per (row, 8-feature group).
+// Pass 2: x * 2^s = hi + lo in fp16, in the UMMA layout (8-point x 16-byte
+// core matrices, K-major).  Row-tile operand opA: block (tile t, slice k) at
+// (t * nk + k) * 32 KB (hi | lo), points permuted by g2_perm_inv.  Column
+// operand opB: per slice, all points in natural order as 1 KB 8-point groups
+// (hi array, then lo array, g.bslice bytes each, one zero group past the last
+// tile).  One thread per (point, 8-feature group); padding is zero.
 __global__ void gram_split_kernel(const float* __restrict__ pts, uint64_t n, uint64_t n_pad, uint32_t d,
-                                  uint32_t nk, const unsigned int* __restrict__ maxbits,
-                                  uint8_t* __restrict__ opA, uint8_t* __restrict__ opB) {
+                                  uint32_t nk, const unsigned int* __restrict__ maxbits, uint8_t* __restrict__ opA,
+                                  uint8_t* __restrict__ opB, uint64_t bslice) {
     const float sc = exp2f((float)g2_scale_exp(__ldg(maxbits)));
     const uint32_t groups = nk * 8;
-    const uint64_t total = n_pad * groups;
+    const uint64_t total = (n_pad + 8) * groups;
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < total;
          v += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t row = v / groups;
@@ -432,32 +484,53 @@ __global__ void gram_split_kernel(const float* __restrict__ pts, uint64_t n, uin
             hi[t] = __float2half_rn(x);
             lo[t] = __float2half_rn(__fsub_rn(x, __half2float(hi[t])));
         }
-        const uint64_t t = row / kGT;
-        const uint32_t r = (uint32_t)(row % kGT), slice = g / 8, kk = (g % 8) * 8;
-        const uint64_t blk = (t * nk + slice) * (uint64_t)kG2Slice;
         const uint4 vh = *reinterpret_cast<const uint4*>(hi), vl = *reinterpret_cast<const uint4*>(lo);
-        const uint32_t ob = g2_off(r, kk), oa = g2_off(g2_perm_inv(r), kk);
-        *reinterpret_cast<uint4*>(opB + blk + ob) = vh;
-        *reinterpret_cast<uint4*>(opB + blk + kG2Half + ob) = vl;
-        *reinterpret_cast<uint4*>(opA + blk + oa) = vh;
-        *reinterpret_cast<uint4*>(opA + blk + kG2Half + oa) = vl;
+        const uint32_t slice = g / 8, kk = (g % 8) * 8;
+        uint8_t* b = opB + slice * 2 * bslice + (row >> 3) * kG2Group + (kk >> 3) * kG2LBO + (row & 7) * 16;
+        *reinterpret_cast<uint4*>(b) = vh;
+        *reinterpret_cast<uint4*>(b + bslice) = vl;
+        if (row < n_pad) {
+            const uint64_t t = row / kGT;
+            uint8_t* blk = opA + (t * nk + slice) * (uint64_t)kG2Slice + g2_off(g2_perm_inv((uint32_t)(row % kGT)), kk);
+            *reinterpret_cast<uint4*>(blk) = vh;
+            *reinterpret_cast<uint4*>(blk + kG2Half) = vl;
+        }
     }
 }
 
-// Realign 64 row values onto 17 aligned chunks (segment start at position A
-// of chunk 0) and stage them: chunk c holds positions 4c - A + [0, 4).
-template <int A>
-__device__ __forceinline__ void g2_stage_row(const float* v, float4* row_buf) {
+__device__ __forceinline__ void g2_ld8(uint32_t taddr, uint32_t* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+
+// d for the 32 owned columns S .. S+31 of the loaded 40 (S = warp-uniform
+// shift): d^2 = |x_i|^2 + |x_j|^2 - 2 * 2^-2s * acc, clamped at 0, sqrt.approx
+template <int S>
+__device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, float ni, float m2, float* dv) {
+    const float2 m22 = make_float2(m2, m2), ni2 = make_float2(ni, ni);
 #pragma unroll
-    for (int c = 0; c < kG2Chunks; ++c) {
-        float e[4];
+    for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 nj = nb4[c4];  // broadcast
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int p = 4 * c - A + t;
-            e[t] = (p >= 0 && p < 64) ? v[p] : 0.0f;
+        for (int t = 0; t < 4; t += 2) {
+            const int p = 4 * c4 + t;
+            const float2 acc = make_float2(__uint_as_float(v[S + p]), __uint_as_float(v[S + p + 1]));
+            const float2 nn = __fadd2_rn(ni2, t == 0 ? make_float2(nj.x, nj.y) : make_float2(nj.z, nj.w));
+            const float2 d2 = __ffma2_rn(acc, m22, nn);
+            float d0, d1;
+            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(fmaxf(d2.x, 0.0f)));
+            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(fmaxf(d2.y, 0.0f)));
+            dv[p] = d0;
+            dv[p + 1] = d1;
         }
-        row_buf[c] = make_float4(e[0], e[1], e[2], e[3]);
     }
+}
+
+__device__ __forceinline__ float g2_dist(uint32_t accbits, float ni, float nj, float m2) {
+    float dd;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(dd) : "f"(fmaxf(fmaf(__uint_as_float(accbits), m2, __fadd_rn(ni, nj)), 0.0f)));
+    return dd;
 }
 
 __global__ void __launch_bounds__(kG2Threads, 1)
@@ -466,12 +539,14 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                      const unsigned int* __restrict__ maxbits, float* __restrict__ out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t nk = g.nk, R = g.ring;
-    uint8_t* sA = smem;                                   // nk x 32 KB
-    uint8_t* sB = smem + nk * kG2Slice;                   // R x 32 KB
-    uint8_t* sE = sB + R * kG2Slice;                      // 8 x kG2EpiBytes
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sE + 8 * kG2EpiBytes);
-    // barrier slots: 0 a_full, 1 a_empty, 2..3 acc_full, 4..5 acc_empty, 6.. b_full[R], 6+R.. b_empty[R]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * R);
+    uint8_t* sA = smem;                                   // row tile: nk x 32 KB (MMA A)
+    uint8_t* sB = smem + nk * kG2Slice;                   // column stages: R x (hi | lo) 17 KB (MMA B)
+    uint8_t* sE = sB + R * kG2Stage;                      // kG2EpiWarps x kG2EpiBytes
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sE + kG2EpiWarps * kG2EpiBytes);
+    // barrier slots: 0 a_full, 1 a_empty, then acc_full[kG2Acc], acc_empty[kG2Acc], b_full[R], b_empty[R]
+    constexpr uint32_t AF = 2, AE = 2 + kG2Acc, BF = 2 + 2 * kG2Acc;
+    const uint32_t BE = BF + R;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + BF + 2 * R);
     const uint32_t bar0 = smem_u32(bars);
     auto BAR = [&](uint32_t k) { return bar0 + 8 * k; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -479,16 +554,16 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     if (threadIdx.x == 0) {
         mbar_init(BAR(0), 1);
         mbar_init(BAR(1), 1);
-        mbar_init(BAR(2), 1);
-        mbar_init(BAR(3), 1);
-        mbar_init(BAR(4), 8);
-        mbar_init(BAR(5), 8);
-        for (uint32_t s = 0; s < 2 * R; ++s) mbar_init(BAR(6 + s), 1);
+        for (uint32_t b = 0; b < kG2Acc; ++b) {
+            mbar_init(BAR(AF + b), 1);
+            mbar_init(BAR(AE + b), kG2EpiWarps);
+        }
+        for (uint32_t s = 0; s < 2 * R; ++s) mbar_init(BAR(BF + s), 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(256));
+                     "r"(kG2TmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -501,47 +576,59 @@ __global__ void __launch_bounds__(kG2Threads, 1)
 
     if (warp == 0) {
         // ------------------------------------------------------- producer
-        if (lane == 0) {
+        if (lane == 0 && tb < te) {
+            Coord c = ltm_map(tb, kReciprocal, true);  // g(lambda) over the tile triangle
             uint64_t cur = ~0ull;
             uint32_t na = 0, q = 0;
-            for (uint64_t lam = tb; lam < te; ++lam) {
-                const Coord c = ltm_map(lam, kReciprocal, true);
+            for (uint64_t lam = tb; lam < te; ++lam, g2_next(c)) {
                 if (c.i != cur) {
-                    if (na > 0) mbar_wait(BAR(1), (na - 1) & 1);  // MMAs done with the old A
+                    if (na > 0) g2_wait_sleep(BAR(1), (na - 1) & 1);  // MMAs done with the old row tile
                     g2_bulk_load(smem_u32(sA), opA + c.i * nk * (uint64_t)kG2Slice, nk * kG2Slice, BAR(0));
                     cur = c.i;
                     ++na;
                 }
                 for (uint32_t k = 0; k < nk; ++k, ++q) {
                     const uint32_t s = q % R, round = q / R;
-                    mbar_wait(BAR(6 + R + s), (round & 1) ^ 1);
-                    g2_bulk_load(smem_u32(sB + s * kG2Slice), opB + (c.j * nk + k) * (uint64_t)kG2Slice, kG2Slice,
-                                 BAR(6 + s));
+                    g2_wait_sleep(BAR(BE + s), (round & 1) ^ 1);
+                    const uint8_t* src = opB + k * 2 * g.bslice + c.j * 16 * (uint64_t)kG2Group;
+                    const uint32_t dst = smem_u32(sB + s * kG2Stage), bar = BAR(BF + s);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kG2Stage)
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dst),
+                        "l"(src), "r"(kG2BHalf), "r"(bar)
+                        : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dst + kG2BHalf),
+                        "l"(src + g.bslice), "r"(kG2BHalf), "r"(bar)
+                        : "memory");
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA
-        if (lane == 0) {
+        if (lane == 0 && tb < te) {
+            Coord c = ltm_map(tb, kReciprocal, true);
             uint64_t cur = ~0ull;
             uint32_t na = 0, q = 0, it = 0;
             for (uint64_t lam = tb; lam < te; ++lam, ++it) {
-                const Coord c = ltm_map(lam, kReciprocal, true);
                 if (c.i != cur) {
-                    mbar_wait(BAR(0), na & 1);
+                    g2_wait_sleep(BAR(0), na & 1);
                     cur = c.i;
                     ++na;
                 }
-                const uint32_t buf = it & 1;
-                mbar_wait(BAR(4 + buf), ((it >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+                const uint32_t buf = it % kG2Acc;
+                g2_wait_sleep(BAR(AE + buf), ((it / kG2Acc) & 1) ^ 1);  // epilogue drained this accumulator
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t dtm = tmem + buf * kGT;
+                const uint32_t dtm = tmem + buf * kG2AccStride;
                 for (uint32_t k = 0; k < nk; ++k, ++q) {
                     const uint32_t s = q % R, round = q / R;
-                    mbar_wait(BAR(6 + s), round & 1);
+                    g2_wait_sleep(BAR(BF + s), round & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t ah = smem_u32(sA + k * kG2Slice), al = ah + kG2Half;
-                    const uint32_t bh = smem_u32(sB + s * kG2Slice), bl = bh + kG2Half;
+                    const uint32_t bh = smem_u32(sB + s * kG2Stage), bl = bh + kG2BHalf;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint32_t ko = kk * 2 * kG2LBO;  // K = 16 fp16 = 2 core matrices
@@ -549,116 +636,114 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                         g2_mma(dtm, g2_desc(al + ko), g2_desc(bh + ko), 1u);
                         g2_mma(dtm, g2_desc(ah + ko), g2_desc(bh + ko), 1u);
                     }
-                    g2_commit(BAR(6 + R + s));  // stage s free once these MMAs complete
+                    g2_commit(BAR(BE + s));  // stage s free once these MMAs complete
                 }
-                g2_commit(BAR(2 + buf));  // accumulator ready
-                bool last_of_row = lam + 1 >= te;
-                if (!last_of_row) last_of_row = ltm_map(lam + 1, kReciprocal, true).i != c.i;
-                if (last_of_row) g2_commit(BAR(1));  // A free
+                g2_commit(BAR(AF + buf));  // accumulator ready
+                const uint64_t row = c.i;
+                g2_next(c);
+                if (lam + 1 >= te || c.i != row) g2_commit(BAR(1));  // row tile free
             }
         }
     } else {
         // ------------------------------------------------------- epilogue
-        const uint32_t q = warp & 3, h = (warp - 2) >> 2;
+        const uint32_t e = warp - 2, q = warp & 3, w4 = e >> 2;
+        const uint32_t a = (q - (uint32_t)g.e_base) & 3u;  // (T(i) + j0 - e_base) mod 4, rows of quarter q
+        const uint32_t s = (4u - a) & 3u;                    // first owned column of every row
         const int sh = g2_scale_exp(__ldg(maxbits));
         const float m2 = -2.0f * exp2f((float)(-2 * sh));
-        const uint32_t a = (uint32_t)(q - (uint32_t)g.e_base) & 3u;  // warp-uniform alignment shift
-        float4* wbuf = reinterpret_cast<float4*>(sE + (warp - 2) * kG2EpiBytes);
-        const uint32_t r_lane = g2_perm(32 * q + lane);
+        float4* wbuf = reinterpret_cast<float4*>(sE + e * kG2EpiBytes);
+        float* nbuf = reinterpret_cast<float*>(sE + e * kG2EpiBytes + 32 * kG2RowChunks * 16);
+        const float4* nb4 = reinterpret_cast<const float4*>(nbuf);
+        const uint32_t r_lane = g2_perm(32 * q + lane);  // compute phase: lane = TMEM lane
+        // store phase: lane -> (row slot 4t + l3, chunk ch); row slot 4t + l3 is tile row 16t + rho_l
+        const uint32_t l3 = lane >> 3, ch = lane & 7;
+        const uint32_t rho_l = g2_perm(32 * q + l3);
+        const float4* rd = wbuf + l3 * kG2RowChunks + ch;
+        float4* my = wbuf + lane * kG2RowChunks;
+        float4* out4 = reinterpret_cast<float4*>(out);
+        const uint32_t cw = 32 * w4 + s;  // first owned column of this warp, relative to the tile
+
+        Coord c = ltm_map(tb, kReciprocal, true);
+        float njp = 0.0f, ni = 0.0f;
+        if (tb < te) {  // norms are zero-padded past the last tile
+            njp = __ldg(norms + c.j * kGT + cw + lane);
+            ni = __ldg(norms + c.i * kGT + r_lane);
+        }
         uint32_t it = 0;
         for (uint64_t lam = tb; lam < te; ++lam, ++it) {
-            const Coord c = ltm_map(lam, kReciprocal, true);
             const uint64_t ri = c.i * kGT, rj = c.j * kGT;
-            const uint32_t buf = it & 1;
-            mbar_wait(BAR(2 + buf), (it >> 1) & 1);
+            const uint32_t buf = it % kG2Acc;
+            nbuf[lane] = njp;  // this tile's 32 column norms -> per-warp smem (broadcast reads)
+            __syncwarp();
+            g2_wait_sleep(BAR(AF + buf), (it / kG2Acc) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            uint32_t v[64];
-            const uint32_t taddr = tmem + ((32 * q) << 16) + buf * kGT + 64 * h;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                : "r"(taddr));
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]),
-                  "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]),
-                  "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]),
-                  "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]),
-                  "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
-                : "r"(taddr + 32));
+            uint32_t v[40];
+            const uint32_t taddr = tmem + ((32 * q) << 16) + buf * kG2AccStride + 32 * w4;
+            g2_ld32(taddr, v);
+            g2_ld8(taddr + 32, v + 32);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
-            if (lane == 0) g2_arrive(BAR(4 + buf));  // TMEM buffer may be overwritten
+            if (lane == 0) g2_arrive(BAR(AE + buf));  // TMEM buffer may be overwritten
 
             const uint64_t i = ri + r_lane;
-            const uint64_t j0 = rj + 64 * h;
-            const bool special = c.i == c.j || ri + kGT > g.n || ri < g.r0 || ri + kGT > g.r1;
-            const float ni = __ldg(norms + i);  // norms are zero-padded to whole tiles
-            float dv[64];
-            const float4* nj4 = reinterpret_cast<const float4*>(norms + j0);
-#pragma unroll
-            for (int c4 = 0; c4 < 16; ++c4) {
-                const float4 nj = __ldg(nj4 + c4);
-                const float njv[4] = {nj.x, nj.y, nj.z, nj.w};
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float d2 = fmaf(__uint_as_float(v[4 * c4 + t]), m2, __fadd_rn(ni, njv[t]));
-                    float dd;
-                    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(dd) : "f"(fmaxf(d2, 0.0f)));
-                    dv[4 * c4 + t] = dd;
-                }
+            // masked tiles: diagonal, its left neighbour (spill columns reach the
+            // diagonal / the next row), rows past n or outside the window
+            const bool special = c.i <= c.j + 1 || ri + kGT > g.n || ri < g.r0 || ri + kGT > g.r1;
+            float dv[32];
+            switch (s) {
+                case 0: g2_epi<0>(v, nb4, ni, m2, dv); break;
+                case 1: g2_epi<1>(v, nb4, ni, m2, dv); break;
+                case 2: g2_epi<2>(v, nb4, ni, m2, dv); break;
+                default: g2_epi<3>(v, nb4, ni, m2, dv); break;
             }
             if (special) {
 #pragma unroll
-                for (int cc = 0; cc < 64; ++cc)
-                    if (j0 + cc == i) dv[cc] = 0.0f;
+                for (int p = 0; p < 32; ++p)
+                    if (rj + cw + p == i) dv[p] = 0.0f;
             }
-            float4* my = wbuf + lane * kG2Chunks;
-            switch (a) {
-                case 0: g2_stage_row<0>(dv, my); break;
-                case 1: g2_stage_row<1>(dv, my); break;
-                case 2: g2_stage_row<2>(dv, my); break;
-                default: g2_stage_row<3>(dv, my); break;
+            if (c.j == 0 && w4 == 0 && s > 0 && i < g.n && i >= g.r0 && i < g.r1) {
+                // columns [0, s) of row i precede its first owned chunk
+                float* rowp = out + (i * (i + 1) / 2 - g.e_base);
+                for (uint32_t p = 0; p < s && p <= i; ++p)
+                    rowp[p] = (p == i) ? 0.0f : g2_dist(v[p], ni, __ldg(norms + p), m2);
             }
-            // float4 index of chunk 0 of this lane's row segment
-            const uint64_t kbase = (i * (i + 1) / 2 + j0 - g.e_base - a) >> 2;
-            __syncwarp();
-#pragma unroll 1
-            for (int s = 0; s < kG2Chunks; ++s) {
-                const uint32_t idx = 32 * s + lane;
-                const uint32_t row = idx / kG2Chunks, cch = idx - row * kG2Chunks;
-                const float4 val = wbuf[idx];
-                const uint64_t kb = __shfl_sync(0xffffffffu, (unsigned long long)kbase, row);
-                const uint64_t ii = ri + g2_perm(32 * q + row);
-                float* dst = out + 4 * (kb + cch);
-                const int p0 = 4 * (int)cch - (int)a;  // segment position of element 0
-                bool ok[4];
-                bool all = true;
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int p = p0 + t;
-                    bool o = p >= 0 && p < 64;
-                    if (special) {
-                        const uint64_t jj = j0 + (uint64_t)p;
-                        o = o && jj <= ii && ii < g.n && ii >= g.r0 && ii < g.r1;
-                    }
-                    ok[t] = o;
-                    all = all && o;
+            for (int cc = 0; cc < 8; ++cc) my[cc] = make_float4(dv[4 * cc], dv[4 * cc + 1], dv[4 * cc + 2], dv[4 * cc + 3]);
+            // prefetch the next tile's norms (latency hidden behind the stores)
+            const Coord cn = c;
+            g2_next(c);
+            if (lam + 1 < te) {
+                njp = __ldg(norms + c.j * kGT + cw + lane);
+                ni = __ldg(norms + c.i * kGT + r_lane);
+            }
+            __syncwarp();
+            if (!special) {
+                // iteration t: rows 16t + rho_l, chunk ch; T(x + 16) - T(x) = 16x + 136
+                uint32_t x = (uint32_t)(ri + rho_l);
+                const uint64_t e0 = (uint64_t)x * (x + 1) / 2 + rj + cw - g.e_base;  // = 0 mod 4
+                float4* p0 = out4 + (e0 >> 2) + ch;
+                uint32_t koff = 0;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    p0[koff] = rd[4 * kG2RowChunks * t];
+                    koff += 4 * x + 34;
+                    x += 16;
                 }
-                if (all) {
-                    *reinterpret_cast<float4*>(dst) = val;
-                } else {
-                    if (ok[0]) dst[0] = val.x;
-                    if (ok[1]) dst[1] = val.y;
-                    if (ok[2]) dst[2] = val.z;
-                    if (ok[3]) dst[3] = val.w;
+            } else {
+                const uint64_t rjc = cn.j * kGT + cw + 4 * ch;  // first column of this lane's chunk
+#pragma unroll 1
+                for (int t = 0; t < 8; ++t) {
+                    const uint64_t ii = cn.i * kGT + 16 * t + rho_l;
+                    if (ii >= g.n || ii < g.r0 || ii >= g.r1 || rjc > ii) continue;
+                    const float4 val = rd[4 * kG2RowChunks * t];
+                    float* dst = out + (ii * (ii + 1) / 2 + rjc - g.e_base);
+                    if (rjc + 3 <= ii) {
+                        *reinterpret_cast<float4*>(dst) = val;
+                    } else {
+                        const float vals[4] = {val.x, val.y, val.z, val.w};
+                        for (uint32_t u = 0; u < 4 && rjc + u <= ii; ++u) dst[u] = vals[u];
+                    }
                 }
             }
             __syncwarp();
@@ -668,7 +753,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kG2TmemCols));
     }
 }
 

@@ -429,30 +429,33 @@ tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, ui
                            const float* pts, float* out, DeviceCtx* c, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        TG_CUDA(cudaFuncSetAttribute(gram2_edm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+        TG_CUDA(cudaFuncSetAttribute(gram2_edm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2SmemMax));
         attr = true;
     }
     const uint64_t r0 = std::min<uint64_t>(n, b0 * rho), r1 = std::min<uint64_t>(n, b1 * rho);
     if (r1 <= r0) return TG_OK;
     const uint32_t nk = (uint32_t)ceil_div(d, 64);
     const uint64_t nt = ceil_div(n, kGT), n_pad = nt * kGT;
-    const uint64_t op_bytes = nt * nk * (uint64_t)kG2Slice;
-    TG_TRY(ensure_buf(c->bufs[4], n_pad * sizeof(float)));
-    TG_TRY(ensure_buf(c->bufs[5], 2 * op_bytes + 256));
+    const uint64_t a_bytes = nt * nk * (uint64_t)kG2Slice;
+    const uint64_t bslice = (nt * 16 + 1) * (uint64_t)kG2Group;
+    const uint64_t b_bytes = nk * 2 * bslice;
+    TG_TRY(ensure_buf(c->bufs[4], (n_pad + 8) * sizeof(float)));
+    TG_TRY(ensure_buf(c->bufs[5], a_bytes + b_bytes + 256));
     float* norms = static_cast<float*>(c->bufs[4].p);
     uint8_t* opA = static_cast<uint8_t*>(c->bufs[5].p);
-    uint8_t* opB = opA + op_bytes;
-    unsigned int* maxbits = reinterpret_cast<unsigned int*>(opB + op_bytes);
+    uint8_t* opB = opA + a_bytes;
+    unsigned int* maxbits = reinterpret_cast<unsigned int*>(opB + b_bytes);
     TG_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned int), st));
-    const unsigned pb = (unsigned)std::min<uint64_t>(ceil_div(n_pad, 256), (uint64_t)c->sms * 8);
-    gram_prep_kernel<<<pb, 256, 0, st>>>(pts, n, n_pad, d, norms, maxbits);
-    const unsigned sb = (unsigned)std::min<uint64_t>(ceil_div(n_pad * nk * 8, 256), (uint64_t)c->sms * 16);
-    gram_split_kernel<<<sb, 256, 0, st>>>(pts, n, n_pad, d, nk, maxbits, opA, opB);
+    const unsigned pb = (unsigned)std::min<uint64_t>(ceil_div(n_pad + 8, 256), (uint64_t)c->sms * 8);
+    gram_prep_kernel<<<pb, 256, 0, st>>>(pts, n, n_pad + 8, d, norms, maxbits);
+    const unsigned sb = (unsigned)std::min<uint64_t>(ceil_div((n_pad + 8) * nk * 8, 256), (uint64_t)c->sms * 16);
+    gram_split_kernel<<<sb, 256, 0, st>>>(pts, n, n_pad, d, nk, maxbits, opA, opB, bslice);
     Gram2Geom g{};
     g.n = n;
     g.nk = nk;
-    const uint64_t fixed = 8ull * kG2EpiBytes + 256;
-    g.ring = (uint32_t)std::min<uint64_t>(4, (232448 - fixed - nk * (uint64_t)kG2Slice) / kG2Slice);
+    g.bslice = bslice;
+    g.ring = 2;
+    while (g.ring < 8 && g2_smem_bytes(nk, g.ring + 1) <= kG2SmemMax) ++g.ring;
     const uint64_t ty0 = r0 / kGT, ty1 = ceil_div(r1, kGT);
     g.t0 = tri(ty0);
     g.t1 = tri(ty1);
@@ -463,9 +466,8 @@ tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, ui
     const uint64_t tiles = g.t1 - g.t0;
     const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)c->sms);
     g.per_cta = ceil_div(tiles, grid);
-    const size_t smem = (nk + g.ring) * (size_t)kG2Slice + 8 * (size_t)kG2EpiBytes + 8 * (6 + 2 * g.ring) + 16;
-    gram2_edm_kernel<<<(unsigned)ceil_div(tiles, g.per_cta), kG2Threads, smem, st>>>(g, opA, opB, norms, maxbits,
-                                                                                     out);
+    gram2_edm_kernel<<<(unsigned)ceil_div(tiles, g.per_cta), kG2Threads, g2_smem_bytes(nk, g.ring), st>>>(
+        g, opA, opB, norms, maxbits, out);
     g_launches += 3;
     TG_CUDA(cudaGetLastError());
     return TG_OK;
