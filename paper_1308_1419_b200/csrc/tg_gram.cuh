@@ -329,7 +329,10 @@ constexpr uint32_t kG2Acc = 3;                // TMEM accumulators
 constexpr uint32_t kG2AccStride = 144;        // TMEM columns per accumulator (>= kG2N)
 constexpr uint32_t kG2TmemCols = 512;
 constexpr int kG2RowChunks = 9;               // staging row stride in 16-byte chunks (8 used, odd: no conflicts)
-constexpr uint32_t kG2EpiBytes = 32 * kG2RowChunks * 16 + 32 * 4;  // per epilogue warp: staging + column norms
+constexpr uint32_t kG2EpiBytes = 32 * kG2RowChunks * 16;  // per epilogue warp: staging
+constexpr uint32_t kG2NormSlots = 4;          // norm ring: [column norms 136 | pad | row norms 128] floats
+constexpr uint32_t kG2NormSlot = (136 + 8 + 128) * 4;
+constexpr uint32_t kG2NormRowOff = (136 + 8) * 4;
 // kind::f16 (A, B fp16, K-major), fp32 accumulate, M = 128, N = 136
 constexpr uint32_t kG2Idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((kG2N >> 3) << 17) |
                               ((uint32_t)(kGT >> 4) << 24);
@@ -346,7 +349,8 @@ struct Gram2Geom {
 };
 
 __host__ __device__ __forceinline__ uint32_t g2_smem_bytes(uint32_t nk, uint32_t ring) {
-    return nk * kG2Slice + ring * kG2Stage + kG2EpiWarps * kG2EpiBytes + 8 * (2 + 2 * kG2Acc + 2 * ring) + 16;
+    return nk * kG2Slice + ring * kG2Stage + kG2EpiWarps * kG2EpiBytes + kG2NormSlots * kG2NormSlot +
+           8 * (2 + 2 * kG2Acc + 2 * ring + 2 * kG2NormSlots) + 16;
 }
 
 // tile row of TMEM lane p (row-tile permutation); quarter q holds T(r) = q mod 4
@@ -505,18 +509,21 @@ __device__ __forceinline__ void g2_ld8(uint32_t taddr, uint32_t* v) {
 }
 
 // d for the 32 owned columns S .. S+31 of the loaded 40 (S = warp-uniform
-// shift): d^2 = |x_i|^2 + |x_j|^2 - 2 * 2^-2s * acc, clamped at 0, sqrt.approx
+// shift): d^2 = |x_i|^2 + |x_j|^2 - 2 * 2^-2s * acc, clamped at 0, sqrt.approx.
+// nb4 = the 16-byte aligned column norms of loaded columns 0 .. 39 (broadcast).
 template <int S>
 __device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, float ni, float m2, float* dv) {
     const float2 m22 = make_float2(m2, m2), ni2 = make_float2(ni, ni);
+    float4 lo = nb4[0];
 #pragma unroll
     for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 nj = nb4[c4];  // broadcast
+        const float4 hi = nb4[c4 + 1];
+        const float w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};  // columns 4 c4 .. 4 c4 + 7
 #pragma unroll
         for (int t = 0; t < 4; t += 2) {
             const int p = 4 * c4 + t;
             const float2 acc = make_float2(__uint_as_float(v[S + p]), __uint_as_float(v[S + p + 1]));
-            const float2 nn = __fadd2_rn(ni2, t == 0 ? make_float2(nj.x, nj.y) : make_float2(nj.z, nj.w));
+            const float2 nn = __fadd2_rn(ni2, make_float2(w[S + t], w[S + t + 1]));
             const float2 d2 = __ffma2_rn(acc, m22, nn);
             float d0, d1;
             asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(fmaxf(d2.x, 0.0f)));
@@ -524,6 +531,7 @@ __device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, flo
             dv[p] = d0;
             dv[p + 1] = d1;
         }
+        lo = hi;
     }
 }
 
@@ -542,9 +550,12 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     uint8_t* sA = smem;                                   // row tile: nk x 32 KB (MMA A)
     uint8_t* sB = smem + nk * kG2Slice;                   // column stages: R x (hi | lo) 17 KB (MMA B)
     uint8_t* sE = sB + R * kG2Stage;                      // kG2EpiWarps x kG2EpiBytes
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sE + kG2EpiWarps * kG2EpiBytes);
-    // barrier slots: 0 a_full, 1 a_empty, then acc_full[kG2Acc], acc_empty[kG2Acc], b_full[R], b_empty[R]
-    constexpr uint32_t AF = 2, AE = 2 + kG2Acc, BF = 2 + 2 * kG2Acc;
+    uint8_t* sN = sE + kG2EpiWarps * kG2EpiBytes;         // norm ring
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sN + kG2NormSlots * kG2NormSlot);
+    // barrier slots: 0 a_full, 1 a_empty, acc_full[kG2Acc], acc_empty[kG2Acc], n_full[NS], n_empty[NS],
+    // b_full[R], b_empty[R]
+    constexpr uint32_t AF = 2, AE = 2 + kG2Acc, NF = 2 + 2 * kG2Acc, NE = NF + kG2NormSlots,
+                       BF = NE + kG2NormSlots;
     const uint32_t BE = BF + R;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + BF + 2 * R);
     const uint32_t bar0 = smem_u32(bars);
@@ -557,6 +568,10 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         for (uint32_t b = 0; b < kG2Acc; ++b) {
             mbar_init(BAR(AF + b), 1);
             mbar_init(BAR(AE + b), kG2EpiWarps);
+        }
+        for (uint32_t b = 0; b < kG2NormSlots; ++b) {
+            mbar_init(BAR(NF + b), 1);
+            mbar_init(BAR(NE + b), kG2EpiWarps);
         }
         for (uint32_t s = 0; s < 2 * R; ++s) mbar_init(BAR(BF + s), 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
@@ -579,8 +594,25 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         if (lane == 0 && tb < te) {
             Coord c = ltm_map(tb, kReciprocal, true);  // g(lambda) over the tile triangle
             uint64_t cur = ~0ull;
-            uint32_t na = 0, q = 0;
-            for (uint64_t lam = tb; lam < te; ++lam, g2_next(c)) {
+            uint32_t na = 0, q = 0, it = 0;
+            for (uint64_t lam = tb; lam < te; ++lam, ++it, g2_next(c)) {
+                {  // norms of the tile: 136 column norms (tile + 8 spill points), 128 row norms
+                    const uint32_t ns = it % kG2NormSlots, bar = BAR(NF + ns);
+                    g2_wait_sleep(BAR(NE + ns), ((it / kG2NormSlots) & 1) ^ 1);
+                    const uint32_t dst = smem_u32(sN + ns * kG2NormSlot);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(136 * 4 + 128 * 4)
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dst),
+                        "l"(norms + c.j * kGT), "r"(136 * 4), "r"(bar)
+                        : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dst + kG2NormRowOff),
+                        "l"(norms + c.i * kGT), "r"(128 * 4), "r"(bar)
+                        : "memory");
+                }
                 if (c.i != cur) {
                     if (na > 0) g2_wait_sleep(BAR(1), (na - 1) & 1);  // MMAs done with the old row tile
                     g2_bulk_load(smem_u32(sA), opA + c.i * nk * (uint64_t)kG2Slice, nk * kG2Slice, BAR(0));
@@ -652,8 +684,6 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         const int sh = g2_scale_exp(__ldg(maxbits));
         const float m2 = -2.0f * exp2f((float)(-2 * sh));
         float4* wbuf = reinterpret_cast<float4*>(sE + e * kG2EpiBytes);
-        float* nbuf = reinterpret_cast<float*>(sE + e * kG2EpiBytes + 32 * kG2RowChunks * 16);
-        const float4* nb4 = reinterpret_cast<const float4*>(nbuf);
         const uint32_t r_lane = g2_perm(32 * q + lane);  // compute phase: lane = TMEM lane
         // store phase: lane -> (row slot 4t + l3, chunk ch); row slot 4t + l3 is tile row 16t + rho_l
         const uint32_t l3 = lane >> 3, ch = lane & 7;
@@ -664,17 +694,15 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         const uint32_t cw = 32 * w4 + s;  // first owned column of this warp, relative to the tile
 
         Coord c = ltm_map(tb, kReciprocal, true);
-        float njp = 0.0f, ni = 0.0f;
-        if (tb < te) {  // norms are zero-padded past the last tile
-            njp = __ldg(norms + c.j * kGT + cw + lane);
-            ni = __ldg(norms + c.i * kGT + r_lane);
-        }
         uint32_t it = 0;
         for (uint64_t lam = tb; lam < te; ++lam, ++it) {
             const uint64_t ri = c.i * kGT, rj = c.j * kGT;
             const uint32_t buf = it % kG2Acc;
-            nbuf[lane] = njp;  // this tile's 32 column norms -> per-warp smem (broadcast reads)
-            __syncwarp();
+            const uint32_t ns = it % kG2NormSlots;
+            const float* nslot = reinterpret_cast<const float*>(sN + ns * kG2NormSlot);
+            g2_wait_sleep(BAR(NF + ns), (it / kG2NormSlots) & 1);
+            const float ni = nslot[kG2NormRowOff / 4 + r_lane];
+            const float4* nb4 = reinterpret_cast<const float4*>(nslot + 32 * w4);  // norms of loaded columns
             g2_wait_sleep(BAR(AF + buf), (it / kG2Acc) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             uint32_t v[40];
@@ -697,26 +725,32 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                 case 2: g2_epi<2>(v, nb4, ni, m2, dv); break;
                 default: g2_epi<3>(v, nb4, ni, m2, dv); break;
             }
+            const bool head = c.j == 0 && w4 == 0 && s > 0;  // warp-uniform
+            float nh0 = 0.0f, nh1 = 0.0f, nh2 = 0.0f;          // column norms 0..2 (head cells)
+            if (head) {
+                nh0 = nslot[0];
+                nh1 = nslot[1];
+                nh2 = nslot[2];
+            }
+            __syncwarp();
+            if (lane == 0) g2_arrive(BAR(NE + ns));  // norm slot consumed
             if (special) {
 #pragma unroll
                 for (int p = 0; p < 32; ++p)
                     if (rj + cw + p == i) dv[p] = 0.0f;
             }
-            if (c.j == 0 && w4 == 0 && s > 0 && i < g.n && i >= g.r0 && i < g.r1) {
+            if (head && i < g.n && i >= g.r0 && i < g.r1) {
                 // columns [0, s) of row i precede its first owned chunk
                 float* rowp = out + (i * (i + 1) / 2 - g.e_base);
-                for (uint32_t p = 0; p < s && p <= i; ++p)
-                    rowp[p] = (p == i) ? 0.0f : g2_dist(v[p], ni, __ldg(norms + p), m2);
+                const float nhv[3] = {nh0, nh1, nh2};
+#pragma unroll
+                for (uint32_t p = 0; p < 3; ++p)
+                    if (p < s && p <= i) rowp[p] = (p == i) ? 0.0f : g2_dist(v[p], ni, nhv[p], m2);
             }
 #pragma unroll
             for (int cc = 0; cc < 8; ++cc) my[cc] = make_float4(dv[4 * cc], dv[4 * cc + 1], dv[4 * cc + 2], dv[4 * cc + 3]);
-            // prefetch the next tile's norms (latency hidden behind the stores)
             const Coord cn = c;
             g2_next(c);
-            if (lam + 1 < te) {
-                njp = __ldg(norms + c.j * kGT + cw + lane);
-                ni = __ldg(norms + c.i * kGT + r_lane);
-            }
             __syncwarp();
             if (!special) {
                 // iteration t: rows 16t + rho_l, chunk ch; T(x + 16) - T(x) = 16x + 136
