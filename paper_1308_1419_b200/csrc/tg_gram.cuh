@@ -329,13 +329,39 @@ constexpr uint32_t kG2Acc = 3;                // TMEM accumulators
 constexpr uint32_t kG2AccStride = 144;        // TMEM columns per accumulator (>= kG2N)
 constexpr uint32_t kG2TmemCols = 512;
 constexpr int kG2RowChunks = 9;               // staging row stride in 16-byte chunks (8 used, odd: no conflicts)
+#ifndef TG_G2_QSTAGE
+#define TG_G2_QSTAGE 1  // 1: the 4 warps of a lane quarter share a 32-row staging tile and store whole rows
+#endif
+#if TG_G2_QSTAGE
+constexpr int kG2QChunks = 33;                // quarter staging row stride (32 used, odd: no conflicts)
+constexpr uint32_t kG2EpiBytes = 32 * kG2QChunks * 16 / 4;  // per epilogue warp (a quarter = 4 warps)
+#else
 constexpr uint32_t kG2EpiBytes = 32 * kG2RowChunks * 16;  // per epilogue warp: staging
-constexpr uint32_t kG2NormSlots = 4;          // norm ring: [column norms 136 | pad | row norms 128] floats
+#endif
+constexpr uint32_t kG2NormSlots = 8;          // norm ring: [column norms 136 | pad | row norms 128] floats
 constexpr uint32_t kG2NormSlot = (136 + 8 + 128) * 4;
 constexpr uint32_t kG2NormRowOff = (136 + 8) * 4;
 // kind::f16 (A, B fp16, K-major), fp32 accumulate, M = 128, N = 136
 constexpr uint32_t kG2Idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((kG2N >> 3) << 17) |
                               ((uint32_t)(kGT >> 4) << 24);
+
+#ifndef TG_G2_PROF
+#define TG_G2_PROF 0
+#endif
+#if TG_G2_PROF
+// A/B instrumentation: cycles spent in each wait (summed over CTAs)
+// 0 prod:norm_empty 1 prod:a_empty 2 prod:b_empty 3 mma:a_full 4 mma:acc_empty 5 mma:b_full
+// 6 epi:norm_full 7 epi:acc_full 8 epi:total 9 mma:total 10 prod:total
+__device__ unsigned long long tg_g2_prof[16];
+#define G2W(slot, call)                                      \
+    do {                                                     \
+        const long long _t0 = clock64();                     \
+        call;                                                \
+        prof[slot] += (unsigned long long)(clock64() - _t0); \
+    } while (0)
+#else
+#define G2W(slot, call) call
+#endif
 
 struct Gram2Geom {
     uint64_t n;
@@ -535,6 +561,11 @@ __device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, flo
     }
 }
 
+// named barrier of the 4 epilogue warps of TMEM lane quarter q (ids 1..4)
+__device__ __forceinline__ void g2_bar_quarter(uint32_t q) {
+    asm volatile("bar.sync %0, 128;" ::"r"(q + 1) : "memory");
+}
+
 __device__ __forceinline__ float g2_dist(uint32_t accbits, float ni, float nj, float m2) {
     float dd;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(dd) : "f"(fmaxf(fmaf(__uint_as_float(accbits), m2, __fadd_rn(ni, nj)), 0.0f)));
@@ -561,6 +592,10 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     const uint32_t bar0 = smem_u32(bars);
     auto BAR = [&](uint32_t k) { return bar0 + 8 * k; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if TG_G2_PROF
+    unsigned long long prof[16] = {};
+    const long long tstart = clock64();
+#endif
 
     if (threadIdx.x == 0) {
         mbar_init(BAR(0), 1);
@@ -598,7 +633,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             for (uint64_t lam = tb; lam < te; ++lam, ++it, g2_next(c)) {
                 {  // norms of the tile: 136 column norms (tile + 8 spill points), 128 row norms
                     const uint32_t ns = it % kG2NormSlots, bar = BAR(NF + ns);
-                    g2_wait_sleep(BAR(NE + ns), ((it / kG2NormSlots) & 1) ^ 1);
+                    G2W(0, g2_wait_sleep(BAR(NE + ns), ((it / kG2NormSlots) & 1) ^ 1));
                     const uint32_t dst = smem_u32(sN + ns * kG2NormSlot);
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(136 * 4 + 128 * 4)
                                  : "memory");
@@ -614,14 +649,14 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                         : "memory");
                 }
                 if (c.i != cur) {
-                    if (na > 0) g2_wait_sleep(BAR(1), (na - 1) & 1);  // MMAs done with the old row tile
+                    if (na > 0) G2W(1, g2_wait_sleep(BAR(1), (na - 1) & 1));  // MMAs done with the old row tile
                     g2_bulk_load(smem_u32(sA), opA + c.i * nk * (uint64_t)kG2Slice, nk * kG2Slice, BAR(0));
                     cur = c.i;
                     ++na;
                 }
                 for (uint32_t k = 0; k < nk; ++k, ++q) {
                     const uint32_t s = q % R, round = q / R;
-                    g2_wait_sleep(BAR(BE + s), (round & 1) ^ 1);
+                    G2W(2, g2_wait_sleep(BAR(BE + s), (round & 1) ^ 1));
                     const uint8_t* src = opB + k * 2 * g.bslice + c.j * 16 * (uint64_t)kG2Group;
                     const uint32_t dst = smem_u32(sB + s * kG2Stage), bar = BAR(BF + s);
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kG2Stage)
@@ -647,17 +682,17 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             uint32_t na = 0, q = 0, it = 0;
             for (uint64_t lam = tb; lam < te; ++lam, ++it) {
                 if (c.i != cur) {
-                    g2_wait_sleep(BAR(0), na & 1);
+                    G2W(3, g2_wait_sleep(BAR(0), na & 1));
                     cur = c.i;
                     ++na;
                 }
                 const uint32_t buf = it % kG2Acc;
-                g2_wait_sleep(BAR(AE + buf), ((it / kG2Acc) & 1) ^ 1);  // epilogue drained this accumulator
+                G2W(4, g2_wait_sleep(BAR(AE + buf), ((it / kG2Acc) & 1) ^ 1));  // epilogue drained this accumulator
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t dtm = tmem + buf * kG2AccStride;
                 for (uint32_t k = 0; k < nk; ++k, ++q) {
                     const uint32_t s = q % R, round = q / R;
-                    g2_wait_sleep(BAR(BF + s), round & 1);
+                    G2W(5, g2_wait_sleep(BAR(BF + s), round & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t ah = smem_u32(sA + k * kG2Slice), al = ah + kG2Half;
                     const uint32_t bh = smem_u32(sB + s * kG2Stage), bl = bh + kG2BHalf;
@@ -683,13 +718,23 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         const uint32_t s = (4u - a) & 3u;                    // first owned column of every row
         const int sh = g2_scale_exp(__ldg(maxbits));
         const float m2 = -2.0f * exp2f((float)(-2 * sh));
+#if TG_G2_QSTAGE
+        // quarter staging tile: row slot r (= TMEM lane 32q + r) x 32 chunks
+        float4* qbuf = reinterpret_cast<float4*>(sE + q * 4 * kG2EpiBytes);
+        float4* wbuf = qbuf;
+#else
         float4* wbuf = reinterpret_cast<float4*>(sE + e * kG2EpiBytes);
+#endif
         const uint32_t r_lane = g2_perm(32 * q + lane);  // compute phase: lane = TMEM lane
         // store phase: lane -> (row slot 4t + l3, chunk ch); row slot 4t + l3 is tile row 16t + rho_l
         const uint32_t l3 = lane >> 3, ch = lane & 7;
         const uint32_t rho_l = g2_perm(32 * q + l3);
         const float4* rd = wbuf + l3 * kG2RowChunks + ch;
+#if TG_G2_QSTAGE
+        float4* my = qbuf + lane * kG2QChunks + 8 * w4;
+#else
         float4* my = wbuf + lane * kG2RowChunks;
+#endif
         float4* out4 = reinterpret_cast<float4*>(out);
         const uint32_t cw = 32 * w4 + s;  // first owned column of this warp, relative to the tile
 
@@ -700,10 +745,10 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             const uint32_t buf = it % kG2Acc;
             const uint32_t ns = it % kG2NormSlots;
             const float* nslot = reinterpret_cast<const float*>(sN + ns * kG2NormSlot);
-            g2_wait_sleep(BAR(NF + ns), (it / kG2NormSlots) & 1);
+            G2W(6, g2_wait_sleep(BAR(NF + ns), (it / kG2NormSlots) & 1));
             const float ni = nslot[kG2NormRowOff / 4 + r_lane];
             const float4* nb4 = reinterpret_cast<const float4*>(nslot + 32 * w4);  // norms of loaded columns
-            g2_wait_sleep(BAR(AF + buf), (it / kG2Acc) & 1);
+            G2W(7, g2_wait_sleep(BAR(AF + buf), (it / kG2Acc) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             uint32_t v[40];
             const uint32_t taddr = tmem + ((32 * q) << 16) + buf * kG2AccStride + 32 * w4;
@@ -747,10 +792,41 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                 for (uint32_t p = 0; p < 3; ++p)
                     if (p < s && p <= i) rowp[p] = (p == i) ? 0.0f : g2_dist(v[p], ni, nhv[p], m2);
             }
+#if TG_G2_QSTAGE
+            g2_bar_quarter(q);  // the quarter's previous tile is fully read
+#endif
 #pragma unroll
             for (int cc = 0; cc < 8; ++cc) my[cc] = make_float4(dv[4 * cc], dv[4 * cc + 1], dv[4 * cc + 2], dv[4 * cc + 3]);
             const Coord cn = c;
             g2_next(c);
+#if TG_G2_QSTAGE
+            g2_bar_quarter(q);  // the quarter's 32 rows x 32 chunks are staged
+            {
+                // warp w4 stores row slots 8 w4 .. 8 w4 + 7, one 512-byte row segment per instruction:
+                // row slot 8 w4 + r is tile row 32 w4 + 8 (r >> 1) + res_q(r & 1)
+                const float4* src = qbuf + 8 * w4 * kG2QChunks + lane;
+                const uint32_t rb0 = g2_perm(32 * q), rb1 = g2_perm(32 * q + 1);
+                const uint64_t colb = rj + s - g.e_base;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const uint64_t ii = ri + 32 * w4 + 8 * (r >> 1) + ((r & 1) ? rb1 : rb0);
+                    const float4 val = src[r * kG2QChunks];
+                    const uint64_t col0 = cn.j * kGT + s + 4 * lane;  // first column of this lane's chunk
+                    if (!special) {
+                        out4[((ii * (ii + 1) / 2 + colb) >> 2) + lane] = val;
+                    } else if (ii < g.n && ii >= g.r0 && ii < g.r1 && col0 <= ii) {
+                        float* dst = out + (ii * (ii + 1) / 2 + col0 - g.e_base);
+                        if (col0 + 3 <= ii) {
+                            *reinterpret_cast<float4*>(dst) = val;
+                        } else {
+                            const float vals[4] = {val.x, val.y, val.z, val.w};
+                            for (uint32_t u = 0; u < 4 && col0 + u <= ii; ++u) dst[u] = vals[u];
+                        }
+                    }
+                }
+            }
+            continue;
+#endif
             __syncwarp();
             if (!special) {
                 // iteration t: rows 16t + rho_l, chunk ch; T(x + 16) - T(x) = 16x + 136
@@ -783,6 +859,13 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             __syncwarp();
         }
     }
+#if TG_G2_PROF
+    if (lane == 0 && (warp <= 2)) {
+        prof[warp == 0 ? 10 : warp == 1 ? 9 : 8] = (unsigned long long)(clock64() - tstart);
+        for (int k = 0; k < 16; ++k)
+            if (prof[k]) atomicAdd(&tg_g2_prof[k], prof[k]);
+    }
+#endif
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 1) {

@@ -1140,3 +1140,19 @@ tg_status tg_gen_points_host(uint64_t n, uint32_t d, uint64_t seed, float* out, 
 }
 
 }  // extern "C"
+
+// A/B instrumentation of the Gram kernel (TG_G2_PROF=1 builds only; zeros otherwise)
+extern "C" int tg_debug_g2_prof(unsigned long long* out16, int reset) {
+#if TG_G2_PROF
+    if (cudaMemcpyFromSymbol(out16, tg::tg_g2_prof, 16 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(tg::tg_g2_prof, z, sizeof(z));
+    }
+    return 0;
+#else
+    for (int k = 0; k < 16; ++k) out16[k] = 0;
+    (void)reset;
+    return 1;
+#endif
+}
