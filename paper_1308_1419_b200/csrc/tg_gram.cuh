@@ -806,15 +806,26 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                 // row slot 8 w4 + r is tile row 32 w4 + 8 (r >> 1) + res_q(r & 1)
                 const float4* src = qbuf + 8 * w4 * kG2QChunks + lane;
                 const uint32_t rb0 = g2_perm(32 * q), rb1 = g2_perm(32 * q + 1);
-                const uint64_t colb = rj + s - g.e_base;
+                if (!special) {
+                    // chunk index of (row x, column rj + s) is (T(x) + rj + s - e_base) / 4
+                    const uint64_t colb = rj + s - g.e_base;
+                    const uint64_t x0 = ri + 32 * w4 + rb0, x1 = ri + 32 * w4 + rb1;
+                    float4* p0 = out4 + ((x0 * (x0 + 1) / 2 + colb) >> 2) + lane;
+                    float4* p1 = out4 + ((x1 * (x1 + 1) / 2 + colb) >> 2) + lane;
+                    // rows x + 8: chunk index + (8x + 36) / 4 = 2x + 9
+                    const uint32_t d0 = 2 * (uint32_t)x0 + 9, d1 = 2 * (uint32_t)x1 + 9;
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const uint64_t ii = ri + 32 * w4 + 8 * (r >> 1) + ((r & 1) ? rb1 : rb0);
-                    const float4 val = src[r * kG2QChunks];
+                    for (int r2 = 0; r2 < 4; ++r2) {
+                        p0[(uint32_t)(r2 * d0 + 8 * r2 * (r2 - 1))] = src[(2 * r2) * kG2QChunks];
+                        p1[(uint32_t)(r2 * d1 + 8 * r2 * (r2 - 1))] = src[(2 * r2 + 1) * kG2QChunks];
+                    }
+                } else {
                     const uint64_t col0 = cn.j * kGT + s + 4 * lane;  // first column of this lane's chunk
-                    if (!special) {
-                        out4[((ii * (ii + 1) / 2 + colb) >> 2) + lane] = val;
-                    } else if (ii < g.n && ii >= g.r0 && ii < g.r1 && col0 <= ii) {
+#pragma unroll 1
+                    for (int r = 0; r < 8; ++r) {
+                        const uint64_t ii = ri + 32 * w4 + 8 * (r >> 1) + ((r & 1) ? rb1 : rb0);
+                        if (ii >= g.n || ii < g.r0 || ii >= g.r1 || col0 > ii) continue;
+                        const float4 val = src[r * kG2QChunks];
                         float* dst = out + (ii * (ii + 1) / 2 + col0 - g.e_base);
                         if (col0 + 3 <= ii) {
                             *reinterpret_cast<float4*>(dst) = val;
