@@ -329,6 +329,9 @@ constexpr uint32_t kG2Acc = 3;                // TMEM accumulators
 constexpr uint32_t kG2AccStride = 144;        // TMEM columns per accumulator (>= kG2N)
 constexpr uint32_t kG2TmemCols = 512;
 constexpr int kG2RowChunks = 9;               // staging row stride in 16-byte chunks (8 used, odd: no conflicts)
+#ifndef TG_G2_SHIFTLD
+#define TG_G2_SHIFTLD 1  // tcgen05.ld at the owned column offset (no realignment moves)
+#endif
 #ifndef TG_G2_QSTAGE
 #define TG_G2_QSTAGE 1  // 1: the 4 warps of a lane quarter share a 32-row staging tile and store whole rows
 #endif
@@ -440,14 +443,29 @@ __device__ __forceinline__ void g2_next(Coord& c) {
 }
 
 // mbarrier wait with a suspend-time hint: a waiting warp sleeps instead of
-// spinning on the issue slots the epilogue warps need
+// spinning on the issue slots the epilogue warps need.  A wait that lasts
+// ~2^34 cycles (seconds) is a pipeline bug: trap instead of hanging the GPU.
 __device__ __forceinline__ void g2_wait_sleep(uint32_t bar, uint32_t phase) {
+    uint32_t done;
     asm volatile(
-        "{\n\t.reg .pred done;\n\t"
-        "WAITS_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
-        "@!done bra WAITS_%=;\n\t}\n" ::"r"(bar),
-        "r"(phase), "r"(0x100000));
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(phase), "r"(0x100000)
+        : "memory");
+    if (done) return;
+    const long long t0 = clock64();
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase), "r"(0x100000)
+            : "memory");
+        if (!done && clock64() - t0 > (1ll << 34)) __trap();
+    } while (!done);
 }
 
 __device__ __forceinline__ void g2_ld32(uint32_t taddr, uint32_t* v) {
@@ -528,6 +546,12 @@ __global__ void gram_split_kernel(const float* __restrict__ pts, uint64_t n, uin
     }
 }
 
+__device__ __forceinline__ void g2_ld4(uint32_t taddr, uint32_t* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr));
+}
+
 __device__ __forceinline__ void g2_ld8(uint32_t taddr, uint32_t* v) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
@@ -537,7 +561,7 @@ __device__ __forceinline__ void g2_ld8(uint32_t taddr, uint32_t* v) {
 // d for the 32 owned columns S .. S+31 of the loaded 40 (S = warp-uniform
 // shift): d^2 = |x_i|^2 + |x_j|^2 - 2 * 2^-2s * acc, clamped at 0, sqrt.approx.
 // nb4 = the 16-byte aligned column norms of loaded columns 0 .. 39 (broadcast).
-template <int S>
+template <int S, int SV = S>
 __device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, float ni, float m2, float* dv) {
     const float2 m22 = make_float2(m2, m2), ni2 = make_float2(ni, ni);
     float4 lo = nb4[0];
@@ -548,7 +572,7 @@ __device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, flo
 #pragma unroll
         for (int t = 0; t < 4; t += 2) {
             const int p = 4 * c4 + t;
-            const float2 acc = make_float2(__uint_as_float(v[S + p]), __uint_as_float(v[S + p + 1]));
+            const float2 acc = make_float2(__uint_as_float(v[SV + p]), __uint_as_float(v[SV + p + 1]));
             const float2 nn = __fadd2_rn(ni2, make_float2(w[S + t], w[S + t + 1]));
             const float2 d2 = __ffma2_rn(acc, m22, nn);
             float d0, d1;
@@ -752,8 +776,14 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             asm volatile("tcgen05.fence::after_thread_sync;");
             uint32_t v[40];
             const uint32_t taddr = tmem + ((32 * q) << 16) + buf * kG2AccStride + 32 * w4;
+#if TG_G2_SHIFTLD
+            // owned columns s + 32 w4 + [0, 32) land in v[s .. s + 31] (the layout g2_epi<s> reads)
+            g2_ld32(taddr + s, v + 0);
+            if (c.j == 0 && w4 == 0 && s > 0) g2_ld4(taddr, v + 32);  // head columns 0..3 (warp-uniform)
+#else
             g2_ld32(taddr, v);
             g2_ld8(taddr + 32, v + 32);
+#endif
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
@@ -764,12 +794,23 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             // diagonal / the next row), rows past n or outside the window
             const bool special = c.i <= c.j + 1 || ri + kGT > g.n || ri < g.r0 || ri + kGT > g.r1;
             float dv[32];
+#if TG_G2_SHIFTLD
+            switch (s) {
+                case 0: g2_epi<0, 0>(v, nb4, ni, m2, dv); break;
+                case 1: g2_epi<1, 0>(v, nb4, ni, m2, dv); break;
+                case 2: g2_epi<2, 0>(v, nb4, ni, m2, dv); break;
+                default: g2_epi<3, 0>(v, nb4, ni, m2, dv); break;
+            }
+            const uint32_t* hvp = v + 32;
+#else
             switch (s) {
                 case 0: g2_epi<0>(v, nb4, ni, m2, dv); break;
                 case 1: g2_epi<1>(v, nb4, ni, m2, dv); break;
                 case 2: g2_epi<2>(v, nb4, ni, m2, dv); break;
                 default: g2_epi<3>(v, nb4, ni, m2, dv); break;
             }
+            const uint32_t* hvp = v;
+#endif
             const bool head = c.j == 0 && w4 == 0 && s > 0;  // warp-uniform
             float nh0 = 0.0f, nh1 = 0.0f, nh2 = 0.0f;          // column norms 0..2 (head cells)
             if (head) {
@@ -790,7 +831,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                 const float nhv[3] = {nh0, nh1, nh2};
 #pragma unroll
                 for (uint32_t p = 0; p < 3; ++p)
-                    if (p < s && p <= i) rowp[p] = (p == i) ? 0.0f : g2_dist(v[p], ni, nhv[p], m2);
+                    if (p < s && p <= i) rowp[p] = (p == i) ? 0.0f : g2_dist(hvp[p], ni, nhv[p], m2);
             }
 #if TG_G2_QSTAGE
             g2_bar_quarter(q);  // the quarter's previous tile is fully read
