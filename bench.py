@@ -357,7 +357,10 @@ def run_ours(args):
                 other["C4_edm_n65536_d64_gram_tcgen05"] = {
                     "ms": gm_ms, "elems_per_s": tri(n) / (gm_ms / 1e3),
                     "hbm_gbs": 4 * cells_local / (gm_ms / 1e3) / 1e9,
-                    "tensor_tflops": 3 * 2 * 64 * 128 * 128 * ((n // 128) * (n // 128 + 1) // 2) / (gm_ms / 1e3) / 1e12,
+                    "frac_hbm": 4 * cells_local / (gm_ms / 1e3) / 1e9 / pk["hbm_gbs"],
+                    # tcgen05 kind::f16, 3 products (hi*hi, hi*lo, lo*hi) of M=128 x N=136 x K=64 per tile
+                    "tensor_tflops": 3 * 2 * 64 * 128 * 136 * ((n // 128) * (n // 128 + 1) // 2) / (gm_ms / 1e3) / 1e12,
+                    "kernel": "gram2_edm_kernel (warp-specialised: bulk-copy producer, tcgen05 MMA, 16 epilogue warps)",
                     "bit_exact": False, "tolerance": "|d^2 - d_exact^2| <= 2^-17 (|x_i|^2 + |x_j|^2)"}
             except RuntimeError as exc:
                 other["C4_edm_n65536_d64_gram_tcgen05"] = {"error": str(exc)}
