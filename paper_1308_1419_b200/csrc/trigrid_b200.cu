@@ -196,7 +196,8 @@ struct DeviceCtx {
     unsigned int* flags = nullptr;       // classify verdicts (ring, one per launch)
     unsigned flag_next = 0;
     unsigned long long* scratch = nullptr;  // [0] sink [1] bad [2] first [3] hits
-    Buf bufs[6];  // [0] pts [1] out (host drop-ins) [2] counts [3] gen [4] gram norms [5] gram operands
+    Buf bufs[7];  // [0] pts [1] out (host drop-ins) [2] counts [3] gen [4] gram norms [5] gram operands
+                  // [6] feature-major points (d > 4 span kernel)
     cudaEvent_t ev[34];
 };
 
@@ -362,10 +363,46 @@ tg_status launch_span_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float*
                              : launch_span_edm_p<1>(d, g, ow, pts, out, flag, st, persistent, sms);
 }
 
+// A/B switch: TG_WIDE_V1=1 keeps the first d > 4 kernel (per-run transposed staging).
+bool wide_v1() {
+    static bool v = [] {
+        const char* e = std::getenv("TG_WIDE_V1");
+        return e && std::atoi(e) != 0;
+    }();
+    return v;
+}
+
+// d > 4, version 2: feature-major copy of the points + pipelined two-runs-per-CTA kernel.
+tg_status launch_wide2_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
+                           const unsigned int* flag, cudaStream_t st, bool persistent, int sms, DeviceCtx* c) {
+    const uint64_t n = g.n;
+    const uint64_t n_pad = ceil_div(n + kW2Cols, kW2Cols) * kW2Cols;  // a run's 128 columns / 16 rows stay in range
+    const uint32_t d_pad = (uint32_t)ceil_div(d, kW2K) * kW2K;
+    TG_TRY(ensure_buf(c->bufs[6], (size_t)n_pad * d_pad * sizeof(float)));
+    float* ptsT = static_cast<float*>(c->bufs[6].p);
+    transpose_points_kernel<<<dim3((unsigned)(n_pad / 32), (unsigned)ceil_div(d_pad, 32)), dim3(32, 8), 0, st>>>(
+        pts, n, d, n_pad, d_pad, ptsT);
+    const size_t smem = 2 * kW2GroupFloats * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        TG_CUDA(cudaFuncSetAttribute(wide2_edm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    static int occ = -1;
+    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_edm_kernel, 256, smem);
+    const uint64_t grid = std::min<uint64_t>(ceil_div(g.units, 2), (uint64_t)sms * std::max(occ, 1) * (persistent ? 1 : 64));
+    if (!grid) return TG_OK;
+    wide2_edm_kernel<<<(unsigned)grid, 256, smem, st>>>(g, ow, ptsT, n_pad, d_pad / kW2K, out, flag);
+    g_launches += 2;
+    TG_CUDA(cudaGetLastError());
+    return TG_OK;
+}
+
 // d > 4: CTA-per-run tiled kernel (rho == 16, runs of <= 128 columns).
 tg_status launch_wide_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
-                          const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
+                          const unsigned int* flag, cudaStream_t st, bool persistent, int sms, DeviceCtx* c) {
     if (g.rho != 16 || g.C != 8) return fail(TG_EINVAL, "wide EDM span kernel needs rho == 16");
+    if (!wide_v1()) return launch_wide2_edm(d, g, ow, pts, out, flag, st, persistent, sms, c);
     uint64_t grid = std::min<uint64_t>(g.units, 0x7fffffffull);
     if (persistent) {
         static int occ = -1;
@@ -870,7 +907,7 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
             if (d <= 4) {
                 TG_TRY(launch_span_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms));
             } else {
-                TG_TRY(launch_wide_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms));
+                TG_TRY(launch_wide_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms, c));
             }
         } else {
             TG_TRY(launch_span_write(g, ow, static_cast<uint32_t*>(out), st, o.persistent != 0, c->sms));
