@@ -940,6 +940,15 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
     return TG_OK;
 }
 
+// A/B switch: TG_COLLIDE_V1=1 keeps the first span collision kernel (one pair per lane per word).
+bool collide_v1() {
+    static bool v = [] {
+        const char* e = std::getenv("TG_COLLIDE_V1");
+        return e && std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spheres, float r_max,
                      uint32_t* bits, uint64_t* hits, const tg_launch_opts* opts,
                      tg_dispatch_stats* stats) {
@@ -966,12 +975,21 @@ tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spher
         const uint64_t nb = ceil_div(n, rho);
         const auto rows = shard_rows(nb, G);
         SpanGeom g;
+        // v2: runs of up to 256 columns (8 column slots per lane)
         TG_TRY(plan_span(s, n, rho, rows[o.shard_index], rows[o.shard_index + 1],
-                         std::max<uint32_t>(1, 128 / rho), &g));
+                         std::max<uint32_t>(1, (collide_v1() ? 128 : 256) / rho), &g));
         const uint64_t grid = span_grid(g, o.persistent != 0, c->sms, 8);
-        if (grid) {
+        if (grid && collide_v1()) {
             span_collide_kernel<<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(
                 g, p0, p1, reinterpret_cast<const float4*>(spheres), r_max, bits,
+                reinterpret_cast<unsigned long long*>(hits));
+            ++g_launches;
+            TG_CUDA(cudaGetLastError());
+        } else if (grid) {
+            // partial words at row-segment ends are OR-ed into a zeroed table
+            TG_CUDA(cudaMemsetAsync(bits, 0, ceil_div(p1 - p0, 32) * 4, st));
+            span_collide2_kernel<8><<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(
+                g, p0, reinterpret_cast<const float4*>(spheres), r_max, bits,
                 reinterpret_cast<unsigned long long*>(hits));
             ++g_launches;
             TG_CUDA(cudaGetLastError());

@@ -28,8 +28,19 @@ def main():
     n = a.n
     if a.kernel == "collide":
         sph = tg.gen_values(n * 4, 42).view(n, 4)
+        ts = []
         for _ in range(a.reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             tg.collide(sph, 0.0625, strategy=a.strategy, mode=a.mode)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        if a.time:
+            ts.sort()
+            ms = ts[len(ts) // 2]
+            print(f"collide n={n} {a.strategy} mode={a.mode}: median {ms:.4f} ms "
+                  f"({n * (n - 1) / 2 / ms / 1e9:.1f} G pairs/s) over {a.reps}")
     else:
         out = torch.empty(n * (n + 1) // 2, dtype=torch.float32 if a.kernel == "edm" else torch.int32, device="cuda")
         pts = tg.gen_values(n * a.d, 42).view(n, a.d) if a.kernel == "edm" else None
