@@ -19,10 +19,16 @@ done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches.csv python bench.py --quick --no-cpu --steps 3 --warmup 3 --e2e-steps 1 > gpurun_out/ncu_bench.log 2>&1
 for k in ${NCU_KERNELS}; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_$k python bench.py --quick --no-cpu --steps 3 --warmup 3 --e2e-steps 1 > gpurun_out/ncu_full_$k.log 2>&1
+  for pg in raw details; do ncu -i gpurun_out/prof_$k.ncu-rep --page $pg --csv > gpurun_out/prof_$k.$pg.csv 2>/dev/null; done
+  [ -z "$NCU_KEEP" ] && rm -f gpurun_out/prof_$k.ncu-rep
 done
 IFS=';' read -ra PROFS <<< "${NCU_PROF}"
 for p in "${PROFS[@]}"; do
   k="${p%%|*}"; args="${p#*|}"
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o gpurun_out/prof_$k python scripts/prof_driver.py $args > gpurun_out/ncu_full_$k.log 2>&1
+  # reports are too big to bring back (64 MiB cap): export the pages ncu_summary.py reads
+  for pg in raw details; do ncu -i gpurun_out/prof_$k.ncu-rep --page $pg --csv > gpurun_out/prof_$k.$pg.csv 2>/dev/null; done
+  ncu -i gpurun_out/prof_$k.ncu-rep --page source --csv --print-source=sass > gpurun_out/prof_$k.source.csv 2>/dev/null
+  [ -z "$NCU_KEEP" ] && rm -f gpurun_out/prof_$k.ncu-rep
 done
 ls -la gpurun_out

@@ -44,8 +44,19 @@ METRICS = [
 ]
 
 
+def _page(rep: str, page: str) -> str:
+    """A report page as CSV text: from the .ncu-rep, or from the <prefix>.<page>.csv
+    export gpu_round.sh writes on the GPU box (reports are too big to bring back)."""
+    if rep.endswith(".ncu-rep"):
+        extra = ["--print-source=sass"] if page == "source" else []
+        return subprocess.run(["ncu", "-i", rep, "--page", page, "--csv", *extra], capture_output=True,
+                              text=True).stdout
+    path = f"{rep}.{page}.csv"
+    return open(path).read() if os.path.exists(path) else ""
+
+
 def raw(rep: str):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    out = _page(rep, "raw")
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return None
@@ -57,7 +68,7 @@ def raw(rep: str):
 
 
 def stalls(rep: str):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    out = _page(rep, "details")
     res = []
     for r in csv.reader(io.StringIO(out)):
         if len(r) > 14 and r[11] in ("Warp State Statistics", "Scheduler Statistics", "Compute Workload Analysis",
@@ -85,6 +96,39 @@ def summarise(tag: str, rep: str) -> tuple[str, dict]:
     for sec, met, unit, val in stalls(rep):
         if met:
             lines.append(f"| {sec} | {met} | {unit} | {val} |")
+    stall_cols = [m for m in k if m.startswith("smsp__pcsamp_warps_issue_stalled_") and not m.endswith("not_issued")]
+    samp = []
+    for m in stall_cols:
+        try:
+            samp.append((float(k[m][0].replace(",", "")), m.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+        except ValueError:
+            pass
+    tot = sum(v for v, _ in samp) or 1.0
+    if samp:
+        lines += ["", "## warp stall samples (all warps)", "", "| reason | samples | share |", "|---|---|---|"]
+        for v, nm in sorted(samp, reverse=True)[:10]:
+            lines.append(f"| {nm} | {v:.0f} | {100 * v / tot:.1f}% |")
+    src = _page(rep, "source")
+    if src:
+        rows = list(csv.reader(io.StringIO(src)))
+        hi = next((i for i, r in enumerate(rows) if "Instructions Executed" in r), None)
+        if hi is not None:
+            hdr = rows[hi]
+            ia, ss = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+            agg, tot_i = defaultdict(lambda: [0, 0]), 0
+            for r in rows[hi + 1:]:
+                if len(r) <= max(ia, ss) or not r[ia].isdigit():
+                    continue
+                toks = r[1].strip().split()
+                op = (toks[1] if toks and toks[0].startswith("@") and len(toks) > 1 else (toks[0] if toks else "?"))
+                op = op.split(".")[0]
+                agg[op][0] += int(r[ia])
+                agg[op][1] += int(r[ss] or 0) if r[ss].isdigit() else 0
+                tot_i += int(r[ia])
+            lines += ["", f"## SASS instruction mix ({tot_i} warp instructions executed)", "",
+                      "| opcode | executed | share | stall samples |", "|---|---|---|---|"]
+            for op, (c, st) in sorted(agg.items(), key=lambda x: -x[1][0])[:16]:
+                lines.append(f"| {op} | {c} | {100 * c / max(tot_i, 1):.1f}% | {st} |")
     return "\n".join(lines) + "\n", {"kernel": name, "short": short, **{m: v for m, (v, _) in vals.items()}}
 
 
