@@ -193,6 +193,7 @@ struct DeviceCtx {
     int sms = 148;
     cudaStream_t stream = nullptr;       // internal compute stream (host drop-ins)
     cudaStream_t copy_stream = nullptr;  // D2H pipeline
+    cudaStream_t copy_stream2 = nullptr; // second D2H stream (alternating 256 MB sub-copies)
     unsigned int* flags = nullptr;       // classify verdicts (ring, one per launch)
     unsigned flag_next = 0;
     unsigned long long* scratch = nullptr;  // [0] sink [1] bad [2] first [3] hits
@@ -234,6 +235,7 @@ tg_status get_ctx(int device, DeviceCtx** out) {
         TG_CUDA(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
         TG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         TG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+        TG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream2, cudaStreamNonBlocking));
         TG_CUDA(cudaMalloc(&c.flags, kFlagRing * sizeof(unsigned int)));
         TG_CUDA(cudaMalloc(&c.scratch, 256));
         for (auto& e : c.ev) TG_CUDA(cudaEventCreate(&e));
@@ -1055,7 +1057,7 @@ tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint
         }
         const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * span_slots()) / rho);
         OutWin ow{eb, ee};
-        uint64_t lo = 0;
+        uint64_t lo = 0, sub_k = 0;
         for (uint32_t q = 0; q < Q; ++q) {
             SpanGeom g;
             TG_TRY(plan_span(s, n, rho, pr[q], pr[q + 1], C, &g));
@@ -1064,9 +1066,16 @@ tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint
             const uint64_t piece_end = tri(std::min<uint64_t>(n, pr[q + 1] * rho)) - eb;
             const uint64_t hi = (q + 1 == Q) ? elems : std::min<uint64_t>(elems, (piece_end + 3) & ~3ull);
             if (hi > lo) {
+                // 256 MB sub-copies alternating two streams: 56 vs 52 GB/s for one
+                // 8.6 GB copy on B200 PCIe Gen5 x16 (scripts/d2h_probe.py)
                 TG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev[q], 0));
-                TG_CUDA(cudaMemcpyAsync(out + lo, d_out + lo, (hi - lo) * sizeof(float),
-                                        cudaMemcpyDeviceToHost, c->copy_stream));
+                TG_CUDA(cudaStreamWaitEvent(c->copy_stream2, c->ev[q], 0));
+                constexpr uint64_t kSub = (256ull << 20) / sizeof(float);
+                for (uint64_t a = lo; a < hi; a += kSub) {
+                    const uint64_t bnd = std::min<uint64_t>(hi, a + kSub);
+                    TG_CUDA(cudaMemcpyAsync(out + a, d_out + a, (bnd - a) * sizeof(float), cudaMemcpyDeviceToHost,
+                                            (sub_k++ & 1) ? c->copy_stream2 : c->copy_stream));
+                }
                 lo = hi;
             }
         }
@@ -1079,6 +1088,7 @@ tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint
         TG_CUDA(cudaMemcpyAsync(out, d_out, elems * sizeof(float), cudaMemcpyDeviceToHost, c->copy_stream));
     }
     TG_CUDA(cudaStreamSynchronize(c->copy_stream));
+    TG_CUDA(cudaStreamSynchronize(c->copy_stream2));
     TG_CUDA(cudaStreamSynchronize(st));
     float ms = 0;
     TG_CUDA(cudaEventElapsedTime(&ms, c->ev[32], c->ev[33]));
