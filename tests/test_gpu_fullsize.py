@@ -96,3 +96,63 @@ def test_collide_full_n32768(tg, orc, cuda):
         assert np.array_equal(allbits[b0:b0 + want.size], want), r0
     frac = int(hits.item()) / pairs
     assert 1e-4 < frac < 1e-2  # r_max chosen for ~0.1-1% hits
+
+
+def test_collide_full_n32768_shards_and_rec(tg, orc, cuda):
+    """8-way shard tables concatenate (bitwise, at the shard's pair offsets) to
+    the whole table; REC gives the same table."""
+    import torch
+    n, r_max = 32768, 0.0625
+    sph = torch.from_numpy(orc.gen_points(n, 4, 42)).to(cuda)
+    whole, hits = tg.collide(sph, r_max, strategy="ltm-r")
+    wbits = np.unpackbits(whole.cpu().numpy().view(np.uint8), bitorder="little")
+    rec, hits_rec = tg.collide(sph, r_max, strategy="rec")
+    assert torch.equal(rec, whole) and int(hits_rec) == int(hits)
+    total = 0
+    for g in range(8):
+        part, h = tg.collide(sph, r_max, strategy="ltm-r", shard=(g, 8))
+        p0, p1 = tg.shard_elems(n, 16, g, 8, with_diag=False)
+        pbits = np.unpackbits(part.cpu().numpy().view(np.uint8), bitorder="little")[:p1 - p0]
+        assert np.array_equal(pbits, wbits[p0:p1]), g
+        total += int(h)
+    assert total == int(hits)
+
+
+def test_edm_direct_d64_full_sampled_rows(tg, orc, cuda):
+    """C4 direct path (bit-exact d > 4 kernel) at N=65536, d=64: sampled full
+    rows byte-identical to the oracle; BB gives the same bytes."""
+    import torch
+    n, d = N, 64
+    pts_np = orc.gen_points(n, d, 42)
+    pts = torch.from_numpy(pts_np).to(cuda)
+    out = tg.edm(pts, strategy="ltm-r")
+    rng = np.random.default_rng(64)
+    for r in sorted(set([0, 1, 15, 16, 127, 128, 4095, n - 1] + [int(x) for x in rng.integers(0, n, 10)])):
+        want = orc.edm_rows(pts_np, r, r + 1)
+        got = out[_tri(r):_tri(r + 1)].cpu().numpy()
+        assert got.tobytes() == want.tobytes(), r
+    o2 = tg.edm(pts, strategy="bb")
+    assert torch.equal(o2.view(torch.int32), out.view(torch.int32))
+    del out, o2
+    torch.cuda.empty_cache()
+
+
+def test_edm_c5_n131072_shards_sampled_rows(tg, orc, cuda):
+    """C5: N=131072, d=3 (34.4 GB packed) as 8 lambda-range shards, one at a
+    time: each shard's first / last / sampled rows byte-identical to the oracle."""
+    import torch
+    n = 131072
+    pts_np = orc.gen_points(n, 3, 42)
+    pts = torch.from_numpy(pts_np).to(cuda)
+    rows = tg.shard_rows(n, 16, 8)  # block rows
+    rng = np.random.default_rng(131072)
+    for g in range(8):
+        r0, r1 = min(n, 16 * rows[g]), min(n, 16 * rows[g + 1])
+        part = tg.edm(pts, strategy="ltm-r", shard=(g, 8))
+        assert part.numel() == _tri(r1) - _tri(r0)
+        for r in sorted(set([r0, r1 - 1] + [int(x) for x in rng.integers(r0, r1, 3)])):
+            want = orc.edm_rows(pts_np, r, r + 1)
+            got = part[_tri(r) - _tri(r0):_tri(r + 1) - _tri(r0)].cpu().numpy()
+            assert got.tobytes() == want.tobytes(), (g, r)
+        del part
+        torch.cuda.empty_cache()
