@@ -262,9 +262,28 @@ bool span_eligible(tg_strategy s, uint32_t rho) {
     return (s == TG_BB || is_ltm(s) || s == TG_REC) && rho % 4 == 0 && rho <= 128;
 }
 
-// Geometry for block rows [b0, b1).
+tg_status plan_span_c(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64_t b1, uint32_t C,
+                      SpanGeom* g);
+
+// Units a launch should have at least: ~32 warps' worth per SM.  A small
+// problem planned with the default C (16 blocks per warp) leaves most SMs idle
+// and each warp on a long serial run walk (N=1024 LTM: 133 warps, 56 us vs
+// 15 us for BB), so C shrinks until the launch has this many units.
+constexpr uint64_t kMinSpanUnits = 148 * 32;
+
+// Geometry for block rows [b0, b1); `adaptive` lets C shrink for small problems
+// (the one-CTA-per-run d > 4 kernel needs the fixed C).
 tg_status plan_span(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64_t b1, uint32_t C,
-                    SpanGeom* g) {
+                    SpanGeom* g, bool adaptive = true) {
+    TG_TRY(plan_span_c(s, n, rho, b0, b1, C, g));
+    if (!adaptive || C <= 1 || g->units >= kMinSpanUnits) return TG_OK;
+    const uint64_t blocks = g->units * C;  // upper bound of the launch's grid blocks
+    const uint32_t c2 = (uint32_t)std::max<uint64_t>(1, blocks / kMinSpanUnits);
+    return c2 < C ? plan_span_c(s, n, rho, b0, b1, c2, g) : TG_OK;
+}
+
+tg_status plan_span_c(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64_t b1, uint32_t C,
+                      SpanGeom* g) {
     std::memset(g, 0, sizeof(*g));
     g->one = 1.0f;
     g->rho = rho;
@@ -901,7 +920,7 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
         const bool wide = kernel == TG_KERNEL_EDM && d > 4;
         const int slots = wide ? 1 : (kernel == TG_KERNEL_WRITE ? write_slots() : span_slots());
         const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * slots) / rho);
-        TG_TRY(plan_span(s, n, rho, b0, b1, C, &g));
+        TG_TRY(plan_span(s, n, rho, b0, b1, C, &g, !wide));
         OutWin ow{tri(std::min<uint64_t>(n, b0 * rho)), tri(std::min<uint64_t>(n, b1 * rho))};
         if (kernel == TG_KERNEL_EDM) {
             unsigned int* flag = next_flag(c);
