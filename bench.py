@@ -339,6 +339,29 @@ def run_ours(args):
 
     # ---- the other BASELINE.json configs (parity cases; timed for reference)
     other = {}
+    if not args.quick and world == 1:
+        # C2: write / dummy td-kernel sweep over N, every mapping (I = t_BB / t_strategy)
+        sweep = {}
+        for ns in (1024, 4096, 16384, 65536):
+            wb = torch.empty(tri(ns), dtype=torch.int32, device=dev)
+            row = {}
+            for mode, strats in (("grid", ("bb", "ltm-r", "utm", "rb", "rec")), ("span", ("bb", "ltm-r", "rec"))):
+                for s in strats:
+                    k = 3 if (ns == 65536 and mode == "grid") else 10
+                    w_ms = time_steps(lambda: tg.launch("write", s, ns, out=wb, rho=RHO, mode=mode, stream=stream,
+                                                        sync=False), k, 2)
+                    r = {"write_ms": w_ms, "write_gbs": 4 * tri(ns) / (w_ms / 1e3) / 1e9}
+                    r["dummy_ms"] = time_steps(lambda: tg.launch("dummy", s, ns, rho=RHO, mode=mode, stream=stream,
+                                                                 sync=False), k, 2)
+                    row[f"{mode}/{s}"] = r
+            for key, r in row.items():
+                bbr = row[key.split("/")[0] + "/bb"]
+                r["I_write_vs_bb"] = bbr["write_ms"] / r["write_ms"]
+                if "dummy_ms" in r:
+                    r["I_dummy_vs_bb"] = bbr["dummy_ms"] / r["dummy_ms"]
+            sweep[str(ns)] = row
+            del wb
+        other["C2_write_dummy_sweep"] = sweep
     if not args.quick:
         # C3: collision table N=32768 (bit-packed no-diagonal table + count)
         nc, r_max = 32768, 0.0625

@@ -905,10 +905,11 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
         if (stats) *stats = st_local;
         return TG_OK;
     }
-    const bool body_span = (kernel == TG_KERNEL_EDM && (d <= 4 || rho == 16)) || kernel == TG_KERNEL_WRITE;
+    const bool body_span = (kernel == TG_KERNEL_EDM && (d <= 4 || rho == 16)) || kernel == TG_KERNEL_WRITE ||
+                           kernel == TG_KERNEL_DUMMY;
     const bool span = resolve_span(o, s, rho, body_span);
     if (span && !(body_span && span_eligible(s, rho)))
-        return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec, rho % 4 == 0 and an edm (d<=4) or write body");
+        return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec, rho % 4 == 0 and an edm (d<=4), write or dummy body");
     if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode (bb/ltm-*)");
 
     Timer timer(st, !o.async);
@@ -929,6 +930,14 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
                 TG_TRY(launch_span_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms));
             } else {
                 TG_TRY(launch_wide_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms, c));
+            }
+        } else if (kernel == TG_KERNEL_DUMMY) {
+            auto* sink = o.sink ? static_cast<unsigned long long*>(o.sink) : c->scratch;
+            const uint64_t grid = span_grid(g, o.persistent != 0, c->sms, 8);
+            if (grid) {
+                span_dummy_kernel<<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, sink, o.sentinel);
+                ++g_launches;
+                TG_CUDA(cudaGetLastError());
             }
         } else {
             TG_TRY(launch_span_write(g, ow, static_cast<uint32_t*>(out), st, o.persistent != 0, c->sms));
