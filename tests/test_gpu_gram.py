@@ -55,3 +55,23 @@ def test_gram_c4_full_size_sampled(tg, orc, cuda):
         want = orc.edm_rows(pts_np, r, r + 1).astype(np.float64)
         assert got[r] == 0.0
         assert np.all(np.abs(got ** 2 - want ** 2) <= TOL * (nrm[r] + nrm[: r + 1])), r
+
+
+@pytest.mark.parametrize("kind", ["offset", "mixed_scale", "duplicates", "negative"])
+def test_gram_tolerance_adversarial(tg, orc, cuda, kind):
+    """The stated tolerance on data that stresses the Gram formula: a large
+    common offset (cancellation), points of very different magnitudes (the
+    global fp16 scale), exact duplicates (d = 0 off the diagonal), signs."""
+    n, d = 700, 64
+    pts = orc.gen_points(n, d, 99).astype(np.float64)
+    if kind == "offset":
+        pts = pts + 1000.0
+    elif kind == "mixed_scale":
+        pts[::2] *= 1e3
+        pts[1::2] *= 1e-3
+    elif kind == "duplicates":
+        pts[1::3] = pts[0::3][: pts[1::3].shape[0]]
+    else:
+        pts = pts - 0.5
+    pts = pts.astype(np.float32)
+    _check(orc, pts, _gram(tg, cuda, pts))
