@@ -905,8 +905,11 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
         if (stats) *stats = st_local;
         return TG_OK;
     }
+    // the dummy kernel runs in span form only on request: AUTO keeps the
+    // paper's one-thread-per-cell dummy so the mapping comparison (I vs BB)
+    // of the reference protocol stays within one execution shape
     const bool body_span = (kernel == TG_KERNEL_EDM && (d <= 4 || rho == 16)) || kernel == TG_KERNEL_WRITE ||
-                           kernel == TG_KERNEL_DUMMY;
+                           (kernel == TG_KERNEL_DUMMY && o.mode == TG_MODE_SPAN);
     const bool span = resolve_span(o, s, rho, body_span);
     if (span && !(body_span && span_eligible(s, rho)))
         return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec, rho % 4 == 0 and an edm (d<=4), write or dummy body");
