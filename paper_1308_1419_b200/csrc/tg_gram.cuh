@@ -313,7 +313,10 @@ __global__ void gram_norms_kernel(const float* __restrict__ pts, uint64_t n, uin
 //    columns (warp-uniform compile-time selection of the shift) -> 8 chunks
 //    per row to a per-warp shared buffer -> transposed read -> STG.128, each
 //    warp store instruction 4 rows x 128 contiguous bytes.
-constexpr int kG2EpiWarps = 16;
+#ifndef TG_G2_EPI
+#define TG_G2_EPI 16  // epilogue warps (4 lane quarters x 4 or x 2)
+#endif
+constexpr int kG2EpiWarps = TG_G2_EPI;
 constexpr int kG2Threads = 32 * (2 + kG2EpiWarps);
 constexpr uint32_t kG2Slice = 32768;          // row-tile block of one 64-feature slice: hi | lo fp16
 constexpr uint32_t kG2Half = 16384;
@@ -328,19 +331,8 @@ constexpr uint32_t kG2SmemMax = 232448;
 constexpr uint32_t kG2Acc = 3;                // TMEM accumulators
 constexpr uint32_t kG2AccStride = 144;        // TMEM columns per accumulator (>= kG2N)
 constexpr uint32_t kG2TmemCols = 512;
-constexpr int kG2RowChunks = 9;               // staging row stride in 16-byte chunks (8 used, odd: no conflicts)
-#ifndef TG_G2_SHIFTLD
-#define TG_G2_SHIFTLD 1  // tcgen05.ld at the owned column offset (no realignment moves)
-#endif
-#ifndef TG_G2_QSTAGE
-#define TG_G2_QSTAGE 1  // 1: the 4 warps of a lane quarter share a 32-row staging tile and store whole rows
-#endif
-#if TG_G2_QSTAGE
-constexpr int kG2QChunks = 33;                // quarter staging row stride (32 used, odd: no conflicts)
-constexpr uint32_t kG2EpiBytes = 32 * kG2QChunks * 16 / 4;  // per epilogue warp (a quarter = 4 warps)
-#else
-constexpr uint32_t kG2EpiBytes = 32 * kG2RowChunks * 16;  // per epilogue warp: staging
-#endif
+constexpr int kG2QChunks = 33;                // quarter staging row stride in chunks (32 used, odd: no conflicts)
+constexpr uint32_t kG2EpiBytes = 32 * kG2QChunks * 16 / (kG2EpiWarps / 4);  // per epilogue warp
 constexpr uint32_t kG2NormSlots = 8;          // norm ring: [column norms 136 | pad | row norms 128] floats
 constexpr uint32_t kG2NormSlot = (136 + 8 + 128) * 4;
 constexpr uint32_t kG2NormRowOff = (136 + 8) * 4;
@@ -587,7 +579,7 @@ __device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, flo
 
 // named barrier of the 4 epilogue warps of TMEM lane quarter q (ids 1..4)
 __device__ __forceinline__ void g2_bar_quarter(uint32_t q) {
-    asm volatile("bar.sync %0, 128;" ::"r"(q + 1) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(q + 1), "n"(32 * (kG2EpiWarps / 4)) : "memory");
 }
 
 __device__ __forceinline__ float g2_dist(uint32_t accbits, float ni, float nj, float m2) {
@@ -737,30 +729,21 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         }
     } else {
         // ------------------------------------------------------- epilogue
+        // kG2EpiWarps warps: TMEM lane quarter q = warp % 4 (32 rows), EPW warps
+        // per quarter, warp w4 owns WCOLS columns and stores WROWS row slots.
+        constexpr int EPW = kG2EpiWarps / 4, WCOLS = 128 / EPW, WROWS = 32 / EPW, NH = WCOLS / 32;
         const uint32_t e = warp - 2, q = warp & 3, w4 = e >> 2;
         const uint32_t a = (q - (uint32_t)g.e_base) & 3u;  // (T(i) + j0 - e_base) mod 4, rows of quarter q
         const uint32_t s = (4u - a) & 3u;                    // first owned column of every row
         const int sh = g2_scale_exp(__ldg(maxbits));
         const float m2 = -2.0f * exp2f((float)(-2 * sh));
-#if TG_G2_QSTAGE
-        // quarter staging tile: row slot r (= TMEM lane 32q + r) x 32 chunks
-        float4* qbuf = reinterpret_cast<float4*>(sE + q * 4 * kG2EpiBytes);
-        float4* wbuf = qbuf;
-#else
-        float4* wbuf = reinterpret_cast<float4*>(sE + e * kG2EpiBytes);
-#endif
+        // quarter staging tile: row slot r (= TMEM lane 32q + r) x 33 chunks (32 used)
+        float4* qbuf = reinterpret_cast<float4*>(sE + q * EPW * kG2EpiBytes);
         const uint32_t r_lane = g2_perm(32 * q + lane);  // compute phase: lane = TMEM lane
-        // store phase: lane -> (row slot 4t + l3, chunk ch); row slot 4t + l3 is tile row 16t + rho_l
-        const uint32_t l3 = lane >> 3, ch = lane & 7;
-        const uint32_t rho_l = g2_perm(32 * q + l3);
-        const float4* rd = wbuf + l3 * kG2RowChunks + ch;
-#if TG_G2_QSTAGE
-        float4* my = qbuf + lane * kG2QChunks + 8 * w4;
-#else
-        float4* my = wbuf + lane * kG2RowChunks;
-#endif
+        float4* my = qbuf + lane * kG2QChunks + (WCOLS / 4) * w4;
         float4* out4 = reinterpret_cast<float4*>(out);
-        const uint32_t cw = 32 * w4 + s;  // first owned column of this warp, relative to the tile
+        const uint32_t cw = WCOLS * w4 + s;  // first owned column of this warp, relative to the tile
+        const uint32_t rb0 = g2_perm(32 * q), rb1 = g2_perm(32 * q + 1);  // tile rows of slots 0, 1 (+8 per 2 slots)
 
         Coord c = ltm_map(tb, kReciprocal, true);
         uint32_t it = 0;
@@ -771,19 +754,16 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             const float* nslot = reinterpret_cast<const float*>(sN + ns * kG2NormSlot);
             G2W(6, g2_wait_sleep(BAR(NF + ns), (it / kG2NormSlots) & 1));
             const float ni = nslot[kG2NormRowOff / 4 + r_lane];
-            const float4* nb4 = reinterpret_cast<const float4*>(nslot + 32 * w4);  // norms of loaded columns
+            const float4* nb4 = reinterpret_cast<const float4*>(nslot + WCOLS * w4);  // norms of loaded columns
             G2W(7, g2_wait_sleep(BAR(AF + buf), (it / kG2Acc) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-            uint32_t v[40];
-            const uint32_t taddr = tmem + ((32 * q) << 16) + buf * kG2AccStride + 32 * w4;
-#if TG_G2_SHIFTLD
-            // owned columns s + 32 w4 + [0, 32) land in v[s .. s + 31] (the layout g2_epi<s> reads)
-            g2_ld32(taddr + s, v + 0);
-            if (c.j == 0 && w4 == 0 && s > 0) g2_ld4(taddr, v + 32);  // head columns 0..3 (warp-uniform)
-#else
-            g2_ld32(taddr, v);
-            g2_ld8(taddr + 32, v + 32);
-#endif
+            const bool head = c.j == 0 && w4 == 0 && s > 0;  // warp-uniform: columns [0, s) of tile (i, 0)
+            uint32_t v[WCOLS + 4];
+            const uint32_t taddr = tmem + ((32 * q) << 16) + buf * kG2AccStride + WCOLS * w4;
+            // owned columns s + WCOLS w4 + [0, WCOLS) (tcgen05.ld at the column offset)
+#pragma unroll
+            for (int h = 0; h < NH; ++h) g2_ld32(taddr + 32 * h + s, v + 32 * h);
+            if (head) g2_ld4(taddr, v + WCOLS);  // head columns 0..3
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
@@ -793,26 +773,17 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             // masked tiles: diagonal, its left neighbour (spill columns reach the
             // diagonal / the next row), rows past n or outside the window
             const bool special = c.i <= c.j + 1 || ri + kGT > g.n || ri < g.r0 || ri + kGT > g.r1;
-            float dv[32];
-#if TG_G2_SHIFTLD
-            switch (s) {
-                case 0: g2_epi<0, 0>(v, nb4, ni, m2, dv); break;
-                case 1: g2_epi<1, 0>(v, nb4, ni, m2, dv); break;
-                case 2: g2_epi<2, 0>(v, nb4, ni, m2, dv); break;
-                default: g2_epi<3, 0>(v, nb4, ni, m2, dv); break;
+            float dv[WCOLS];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                switch (s) {
+                    case 0: g2_epi<0, 0>(v + 32 * h, nb4 + 8 * h, ni, m2, dv + 32 * h); break;
+                    case 1: g2_epi<1, 0>(v + 32 * h, nb4 + 8 * h, ni, m2, dv + 32 * h); break;
+                    case 2: g2_epi<2, 0>(v + 32 * h, nb4 + 8 * h, ni, m2, dv + 32 * h); break;
+                    default: g2_epi<3, 0>(v + 32 * h, nb4 + 8 * h, ni, m2, dv + 32 * h); break;
+                }
             }
-            const uint32_t* hvp = v + 32;
-#else
-            switch (s) {
-                case 0: g2_epi<0>(v, nb4, ni, m2, dv); break;
-                case 1: g2_epi<1>(v, nb4, ni, m2, dv); break;
-                case 2: g2_epi<2>(v, nb4, ni, m2, dv); break;
-                default: g2_epi<3>(v, nb4, ni, m2, dv); break;
-            }
-            const uint32_t* hvp = v;
-#endif
-            const bool head = c.j == 0 && w4 == 0 && s > 0;  // warp-uniform
-            float nh0 = 0.0f, nh1 = 0.0f, nh2 = 0.0f;          // column norms 0..2 (head cells)
+            float nh0 = 0.0f, nh1 = 0.0f, nh2 = 0.0f;  // column norms 0..2 (head cells)
             if (head) {
                 nh0 = nslot[0];
                 nh1 = nslot[1];
@@ -822,93 +793,55 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             if (lane == 0) g2_arrive(BAR(NE + ns));  // norm slot consumed
             if (special) {
 #pragma unroll
-                for (int p = 0; p < 32; ++p)
+                for (int p = 0; p < WCOLS; ++p)
                     if (rj + cw + p == i) dv[p] = 0.0f;
             }
             if (head && i < g.n && i >= g.r0 && i < g.r1) {
-                // columns [0, s) of row i precede its first owned chunk
                 float* rowp = out + (i * (i + 1) / 2 - g.e_base);
                 const float nhv[3] = {nh0, nh1, nh2};
 #pragma unroll
                 for (uint32_t p = 0; p < 3; ++p)
-                    if (p < s && p <= i) rowp[p] = (p == i) ? 0.0f : g2_dist(hvp[p], ni, nhv[p], m2);
+                    if (p < s && p <= i) rowp[p] = (p == i) ? 0.0f : g2_dist(v[WCOLS + p], ni, nhv[p], m2);
             }
-#if TG_G2_QSTAGE
             g2_bar_quarter(q);  // the quarter's previous tile is fully read
-#endif
 #pragma unroll
-            for (int cc = 0; cc < 8; ++cc) my[cc] = make_float4(dv[4 * cc], dv[4 * cc + 1], dv[4 * cc + 2], dv[4 * cc + 3]);
+            for (int cc = 0; cc < WCOLS / 4; ++cc)
+                my[cc] = make_float4(dv[4 * cc], dv[4 * cc + 1], dv[4 * cc + 2], dv[4 * cc + 3]);
             const Coord cn = c;
             g2_next(c);
-#if TG_G2_QSTAGE
             g2_bar_quarter(q);  // the quarter's 32 rows x 32 chunks are staged
-            {
-                // warp w4 stores row slots 8 w4 .. 8 w4 + 7, one 512-byte row segment per instruction:
-                // row slot 8 w4 + r is tile row 32 w4 + 8 (r >> 1) + res_q(r & 1)
-                const float4* src = qbuf + 8 * w4 * kG2QChunks + lane;
-                const uint32_t rb0 = g2_perm(32 * q), rb1 = g2_perm(32 * q + 1);
-                if (!special) {
-                    // chunk index of (row x, column rj + s) is (T(x) + rj + s - e_base) / 4
-                    const uint64_t colb = rj + s - g.e_base;
-                    const uint64_t x0 = ri + 32 * w4 + rb0, x1 = ri + 32 * w4 + rb1;
-                    float4* p0 = out4 + ((x0 * (x0 + 1) / 2 + colb) >> 2) + lane;
-                    float4* p1 = out4 + ((x1 * (x1 + 1) / 2 + colb) >> 2) + lane;
-                    // rows x + 8: chunk index + (8x + 36) / 4 = 2x + 9
-                    const uint32_t d0 = 2 * (uint32_t)x0 + 9, d1 = 2 * (uint32_t)x1 + 9;
-#pragma unroll
-                    for (int r2 = 0; r2 < 4; ++r2) {
-                        p0[(uint32_t)(r2 * d0 + 8 * r2 * (r2 - 1))] = src[(2 * r2) * kG2QChunks];
-                        p1[(uint32_t)(r2 * d1 + 8 * r2 * (r2 - 1))] = src[(2 * r2 + 1) * kG2QChunks];
-                    }
-                } else {
-                    const uint64_t col0 = cn.j * kGT + s + 4 * lane;  // first column of this lane's chunk
-#pragma unroll 1
-                    for (int r = 0; r < 8; ++r) {
-                        const uint64_t ii = ri + 32 * w4 + 8 * (r >> 1) + ((r & 1) ? rb1 : rb0);
-                        if (ii >= g.n || ii < g.r0 || ii >= g.r1 || col0 > ii) continue;
-                        const float4 val = src[r * kG2QChunks];
-                        float* dst = out + (ii * (ii + 1) / 2 + col0 - g.e_base);
-                        if (col0 + 3 <= ii) {
-                            *reinterpret_cast<float4*>(dst) = val;
-                        } else {
-                            const float vals[4] = {val.x, val.y, val.z, val.w};
-                            for (uint32_t u = 0; u < 4 && col0 + u <= ii; ++u) dst[u] = vals[u];
-                        }
-                    }
-                }
-            }
-            continue;
-#endif
-            __syncwarp();
+            // warp w4 stores row slots WROWS w4 .. + WROWS, one 512-byte row segment per
+            // instruction: slot 2 r2 + b (relative) is tile row 4 WROWS w4 + 8 r2 + rb_b
+            const float4* src = qbuf + WROWS * w4 * kG2QChunks + lane;
             if (!special) {
-                // iteration t: rows 16t + rho_l, chunk ch; T(x + 16) - T(x) = 16x + 136
-                uint32_t x = (uint32_t)(ri + rho_l);
-                const uint64_t e0 = (uint64_t)x * (x + 1) / 2 + rj + cw - g.e_base;  // = 0 mod 4
-                float4* p0 = out4 + (e0 >> 2) + ch;
-                uint32_t koff = 0;
+                // chunk index of (row x, column rj + s) is (T(x) + rj + s - e_base) / 4;
+                // rows x + 8: + (8x + 36) / 4 = 2x + 9
+                const uint64_t colb = rj + s - g.e_base;
+                const uint64_t x0 = ri + 4 * WROWS * w4 + rb0, x1 = ri + 4 * WROWS * w4 + rb1;
+                float4* p0 = out4 + ((x0 * (x0 + 1) / 2 + colb) >> 2) + lane;
+                float4* p1 = out4 + ((x1 * (x1 + 1) / 2 + colb) >> 2) + lane;
+                const uint32_t d0 = 2 * (uint32_t)x0 + 9, d1 = 2 * (uint32_t)x1 + 9;
 #pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    p0[koff] = rd[4 * kG2RowChunks * t];
-                    koff += 4 * x + 34;
-                    x += 16;
+                for (int r2 = 0; r2 < WROWS / 2; ++r2) {
+                    p0[(uint32_t)(r2 * d0 + 8 * r2 * (r2 - 1))] = src[(2 * r2) * kG2QChunks];
+                    p1[(uint32_t)(r2 * d1 + 8 * r2 * (r2 - 1))] = src[(2 * r2 + 1) * kG2QChunks];
                 }
             } else {
-                const uint64_t rjc = cn.j * kGT + cw + 4 * ch;  // first column of this lane's chunk
+                const uint64_t col0 = cn.j * kGT + s + 4 * lane;  // first column of this lane's chunk
 #pragma unroll 1
-                for (int t = 0; t < 8; ++t) {
-                    const uint64_t ii = cn.i * kGT + 16 * t + rho_l;
-                    if (ii >= g.n || ii < g.r0 || ii >= g.r1 || rjc > ii) continue;
-                    const float4 val = rd[4 * kG2RowChunks * t];
-                    float* dst = out + (ii * (ii + 1) / 2 + rjc - g.e_base);
-                    if (rjc + 3 <= ii) {
+                for (int r = 0; r < WROWS; ++r) {
+                    const uint64_t ii = ri + 4 * WROWS * w4 + 8 * (r >> 1) + ((r & 1) ? rb1 : rb0);
+                    if (ii >= g.n || ii < g.r0 || ii >= g.r1 || col0 > ii) continue;
+                    const float4 val = src[r * kG2QChunks];
+                    float* dst = out + (ii * (ii + 1) / 2 + col0 - g.e_base);
+                    if (col0 + 3 <= ii) {
                         *reinterpret_cast<float4*>(dst) = val;
                     } else {
                         const float vals[4] = {val.x, val.y, val.z, val.w};
-                        for (uint32_t u = 0; u < 4 && rjc + u <= ii; ++u) dst[u] = vals[u];
+                        for (uint32_t u = 0; u < 4 && col0 + u <= ii; ++u) dst[u] = vals[u];
                     }
                 }
             }
-            __syncwarp();
         }
     }
 #if TG_G2_PROF
