@@ -312,17 +312,27 @@ tg_status plan_span_c(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint
         uint32_t k;
         rec_decompose(n, rho, &m, &k);
         g->m = m;
+        // unit order: the diagonal pass and the small low levels first (many short
+        // runs per unit, slow warps) so they do not form the launch's tail; the
+        // big square passes, whose units are uniform full runs, come last
+        // (the passes are independent)
+        // A pass whose squares are narrower than C blocks gets units of one block
+        // row (cu = sb): a unit is then one run instead of C / sb short runs
+        // walked by one warp.
         uint64_t unit = 0;
         int p = 0;
+        const uint64_t sb0 = m / rho;
+        const uint32_t cu0 = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(C, sb0));
+        g->pass[p] = RecPass{unit, sb0 * sb0 * (1ull << k), sb0, m, 0, cu0};
+        unit += ceil_div(g->pass[p].vb_count, cu0);
+        ++p;
         for (uint32_t level = 1; level <= k; ++level, ++p) {
             const uint64_t side = m << (level - 1), sb = side / rho;
-            g->pass[p] = RecPass{unit, sb * sb * (1ull << (k - level)), sb, side, level};
-            unit += ceil_div(g->pass[p].vb_count, C);
+            const uint32_t cu = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(C, sb));
+            g->pass[p] = RecPass{unit, sb * sb * (1ull << (k - level)), sb, side, level, cu};
+            unit += ceil_div(g->pass[p].vb_count, cu);
         }
-        const uint64_t sb = m / rho;
-        g->pass[p] = RecPass{unit, sb * sb * (1ull << k), sb, m, 0};
-        unit += ceil_div(g->pass[p].vb_count, C);
-        g->npass = p + 1;
+        g->npass = p;
         g->units = unit;
         g->vb_count = 0;
     } else {
