@@ -413,7 +413,7 @@ tg_status launch_wide2_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float
     float* ptsT = static_cast<float*>(c->bufs[6].p);
     transpose_points_kernel<<<dim3((unsigned)(n_pad / 32), (unsigned)ceil_div(d_pad, 32)), dim3(32, 8), 0, st>>>(
         pts, n, d, n_pad, d_pad, ptsT);
-    const size_t smem = 2 * kW2GroupFloats * sizeof(float);
+    const size_t smem = kW2Groups * kW2GroupFloats * sizeof(float);
     static bool attr = false;
     if (!attr) {
         TG_CUDA(cudaFuncSetAttribute(wide2_edm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -421,7 +421,8 @@ tg_status launch_wide2_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float
     }
     static int occ = -1;
     if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_edm_kernel, 256, smem);
-    const uint64_t grid = std::min<uint64_t>(ceil_div(g.units, 2), (uint64_t)sms * std::max(occ, 1) * (persistent ? 1 : 64));
+    const uint64_t grid =
+        std::min<uint64_t>(ceil_div(g.units, kW2Groups), (uint64_t)sms * std::max(occ, 1) * (persistent ? 1 : 64));
     if (!grid) return TG_OK;
     wide2_edm_kernel<<<(unsigned)grid, 256, smem, st>>>(g, ow, ptsT, n_pad, d_pad / kW2K, out, flag);
     g_launches += 2;
