@@ -269,16 +269,23 @@ tg_status plan_span_c(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint
 // problem planned with the default C (16 blocks per warp) leaves most SMs idle
 // and each warp on a long serial run walk (N=1024 LTM: 133 warps, 56 us vs
 // 15 us for BB), so C shrinks until the launch has this many units.
-constexpr uint64_t kMinSpanUnits = 148 * 32;
+uint64_t min_span_units() {  // A/B: TG_SPAN_MIN_UNITS
+    static uint64_t v = [] {
+        const char* e = std::getenv("TG_SPAN_MIN_UNITS");
+        return e ? (uint64_t)std::atoll(e) : (uint64_t)148 * 32;
+    }();
+    return v;
+}
 
 // Geometry for block rows [b0, b1); `adaptive` lets C shrink for small problems
 // (the one-CTA-per-run d > 4 kernel needs the fixed C).
 tg_status plan_span(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64_t b1, uint32_t C,
                     SpanGeom* g, bool adaptive = true) {
     TG_TRY(plan_span_c(s, n, rho, b0, b1, C, g));
-    if (!adaptive || C <= 1 || g->units >= kMinSpanUnits) return TG_OK;
+    const uint64_t min_units = min_span_units();
+    if (!adaptive || C <= 1 || g->units >= min_units) return TG_OK;
     const uint64_t blocks = g->units * C;  // upper bound of the launch's grid blocks
-    const uint32_t c2 = (uint32_t)std::max<uint64_t>(1, blocks / kMinSpanUnits);
+    const uint32_t c2 = (uint32_t)std::max<uint64_t>(1, blocks / min_units);
     return c2 < C ? plan_span_c(s, n, rho, b0, b1, c2, g) : TG_OK;
 }
 
