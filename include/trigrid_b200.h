@@ -67,8 +67,8 @@ typedef enum {
     TG_MODE_AUTO = 0, /* span for bb/ltm/rec when rho % 4 == 0 and the body allows (edm, write), else grid */
     TG_MODE_GRID = 1, /* paper-faithful: one CTA of rho*rho threads per grid block, one cell per thread */
     TG_MODE_SPAN = 2, /* B200: warp per run of consecutive blocks, 128-bit owned-chunk stores */
-    TG_MODE_GRAM = 3  /* EDM only: Gram trick on tcgen05 (d <= 128: fp16 hi/lo split, kind::f16;
-                         d > 128: 3xTF32), stated tolerance
+    TG_MODE_GRAM = 3  /* EDM only: Gram trick on tcgen05 (fp16 hi/lo split, kind::f16, any d),
+                         stated tolerance
                          |d^2 - d_exact^2| <= 2^-17 (|x_i|^2 + |x_j|^2), diagonal 0; not bit-exact */
 } tg_mode;
 

@@ -367,10 +367,19 @@ struct Gram2Geom {
     uint64_t r0, r1;    // element rows of the output window
     uint64_t e_base, e_end;
     uint64_t bslice;    // bytes of one slice of the column operand (hi or lo)
+    uint32_t a_stream;  // 0: row tile resident (nk <= kG2MaxNk); 1: row slices ride the ring with the columns
+    uint32_t stage;     // bytes of one ring stage
 };
 
-__host__ __device__ __forceinline__ uint32_t g2_smem_bytes(uint32_t nk, uint32_t ring) {
-    return nk * kG2Slice + ring * kG2Stage + kG2EpiWarps * kG2EpiBytes + kG2NormSlots * kG2NormSlot +
+// ring stage: the column slice (hi | lo, 17 KB each), preceded by the row-tile
+// slice (32 KB) when the row operand streams (d > 64 kG2MaxNk)
+__host__ __device__ __forceinline__ uint32_t g2_stage_bytes(bool a_stream) {
+    return a_stream ? kG2Slice + kG2Stage : kG2Stage;
+}
+
+__host__ __device__ __forceinline__ uint32_t g2_smem_bytes(uint32_t nk, uint32_t ring, bool a_stream = false) {
+    return (a_stream ? 0u : nk * kG2Slice) + ring * g2_stage_bytes(a_stream) + kG2EpiWarps * kG2EpiBytes +
+           kG2NormSlots * kG2NormSlot +
            8 * (2 + 2 * kG2Acc + 2 * ring + 2 * kG2NormSlots) + 16;
 }
 
@@ -594,9 +603,12 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                      const unsigned int* __restrict__ maxbits, float* __restrict__ out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t nk = g.nk, R = g.ring;
-    uint8_t* sA = smem;                                   // row tile: nk x 32 KB (MMA A)
-    uint8_t* sB = smem + nk * kG2Slice;                   // column stages: R x (hi | lo) 17 KB (MMA B)
-    uint8_t* sE = sB + R * kG2Stage;                      // kG2EpiWarps x kG2EpiBytes
+    const bool as = g.a_stream != 0;
+    uint8_t* sA = smem;                                   // resident row tile: nk x 32 KB (MMA A)
+    uint8_t* sB = smem + (as ? 0u : nk * kG2Slice);       // ring: R x ([row slice 32 KB] | col hi | col lo)
+    const uint32_t SB = g.stage;
+    const uint32_t boff = as ? kG2Slice : 0u;             // column slice offset inside a stage
+    uint8_t* sE = sB + R * SB;                            // kG2EpiWarps x kG2EpiBytes
     uint8_t* sN = sE + kG2EpiWarps * kG2EpiBytes;         // norm ring
     uint64_t* bars = reinterpret_cast<uint64_t*>(sN + kG2NormSlots * kG2NormSlot);
     // barrier slots: 0 a_full, 1 a_empty, acc_full[kG2Acc], acc_empty[kG2Acc], n_full[NS], n_empty[NS],
@@ -664,7 +676,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                         "l"(norms + c.i * kGT), "r"(128 * 4), "r"(bar)
                         : "memory");
                 }
-                if (c.i != cur) {
+                if (!as && c.i != cur) {
                     if (na > 0) G2W(1, g2_wait_sleep(BAR(1), (na - 1) & 1));  // MMAs done with the old row tile
                     g2_bulk_load(smem_u32(sA), opA + c.i * nk * (uint64_t)kG2Slice, nk * kG2Slice, BAR(0));
                     cur = c.i;
@@ -674,9 +686,15 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                     const uint32_t s = q % R, round = q / R;
                     G2W(2, g2_wait_sleep(BAR(BE + s), (round & 1) ^ 1));
                     const uint8_t* src = opB + k * 2 * g.bslice + c.j * 16 * (uint64_t)kG2Group;
-                    const uint32_t dst = smem_u32(sB + s * kG2Stage), bar = BAR(BF + s);
-                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kG2Stage)
+                    const uint32_t dst = smem_u32(sB + s * SB) + boff, bar = BAR(BF + s);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(SB)
                                  : "memory");
+                    if (as)  // the row tile's slice k rides along
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                dst - kG2Slice),
+                            "l"(opA + (c.i * nk + k) * (uint64_t)kG2Slice), "r"(kG2Slice), "r"(bar)
+                            : "memory");
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                             dst),
@@ -697,7 +715,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             uint64_t cur = ~0ull;
             uint32_t na = 0, q = 0, it = 0;
             for (uint64_t lam = tb; lam < te; ++lam, ++it) {
-                if (c.i != cur) {
+                if (!as && c.i != cur) {
                     G2W(3, g2_wait_sleep(BAR(0), na & 1));
                     cur = c.i;
                     ++na;
@@ -710,8 +728,8 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                     const uint32_t s = q % R, round = q / R;
                     G2W(5, g2_wait_sleep(BAR(BF + s), round & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint32_t ah = smem_u32(sA + k * kG2Slice), al = ah + kG2Half;
-                    const uint32_t bh = smem_u32(sB + s * kG2Stage), bl = bh + kG2BHalf;
+                    const uint32_t ah = as ? smem_u32(sB + s * SB) : smem_u32(sA + k * kG2Slice), al = ah + kG2Half;
+                    const uint32_t bh = smem_u32(sB + s * SB) + boff, bl = bh + kG2BHalf;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint32_t ko = kk * 2 * kG2LBO;  // K = 16 fp16 = 2 core matrices
@@ -724,7 +742,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                 g2_commit(BAR(AF + buf));  // accumulator ready
                 const uint64_t row = c.i;
                 g2_next(c);
-                if (lam + 1 >= te || c.i != row) g2_commit(BAR(1));  // row tile free
+                if (!as && (lam + 1 >= te || c.i != row)) g2_commit(BAR(1));  // row tile free
             }
         }
     } else {

@@ -499,7 +499,7 @@ bool gram_v1() {
     return v;
 }
 
-// Pipelined fp16-split Gram EDM (tg_gram.cuh v2) for d <= 128: prep (norms,
+// Pipelined fp16-split Gram EDM (tg_gram.cuh v2), any d (row tile resident for d <= 128, streamed above): prep (norms,
 // max |x|) -> split (hi/lo operands in UMMA layout) -> warp-specialised kernel.
 tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, uint64_t b1, OutWin ow,
                            const float* pts, float* out, DeviceCtx* c, cudaStream_t st) {
@@ -530,8 +530,11 @@ tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, ui
     g.n = n;
     g.nk = nk;
     g.bslice = bslice;
+    g.a_stream = nk > (uint32_t)kG2MaxNk ? 1u : 0u;
+    g.stage = g2_stage_bytes(g.a_stream != 0);
     g.ring = 2;
-    while (g.ring < 8 && g2_smem_bytes(nk, g.ring + 1) <= kG2SmemMax) ++g.ring;
+    while (g.ring < 8 && g2_smem_bytes(nk, g.ring + 1, g.a_stream != 0) <= kG2SmemMax) ++g.ring;
+    if (g2_smem_bytes(nk, g.ring, g.a_stream != 0) > kG2SmemMax) return fail(TG_EINVAL, "gram: shared memory plan");
     const uint64_t ty0 = r0 / kGT, ty1 = ceil_div(r1, kGT);
     g.t0 = tri(ty0);
     g.t1 = tri(ty1);
@@ -542,7 +545,7 @@ tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, ui
     const uint64_t tiles = g.t1 - g.t0;
     const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)c->sms);
     g.per_cta = ceil_div(tiles, grid);
-    gram2_edm_kernel<<<(unsigned)ceil_div(tiles, g.per_cta), kG2Threads, g2_smem_bytes(nk, g.ring), st>>>(
+    gram2_edm_kernel<<<(unsigned)ceil_div(tiles, g.per_cta), kG2Threads, g2_smem_bytes(nk, g.ring, g.a_stream != 0), st>>>(
         g, opA, opB, norms, maxbits, out);
     g_launches += 3;
     TG_CUDA(cudaGetLastError());
@@ -912,7 +915,7 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
         const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
         OutWin ow{tri(std::min<uint64_t>(n, b0 * rho)), tri(std::min<uint64_t>(n, b1 * rho))};
         Timer timer(st, !o.async);
-        if (d <= 64 * kG2MaxNk && !gram_v1()) {
+        if (!gram_v1()) {
             TG_TRY(launch_gram2_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out), c, st));
         } else {
             TG_TRY(ensure_buf(c->bufs[4], n * sizeof(float)));

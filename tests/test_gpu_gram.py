@@ -29,7 +29,7 @@ def _check(orc, pts, got):
     return worst
 
 
-@pytest.mark.parametrize("n,d", [(1, 8), (100, 8), (128, 64), (200, 64), (1000, 64), (777, 100), (4096, 64), (300, 3), (300, 200), (513, 128), (130, 65), (260, 256), (200, 300), (2000, 128), (1100, 37)])
+@pytest.mark.parametrize("n,d", [(1, 8), (100, 8), (128, 64), (200, 64), (1000, 64), (777, 100), (4096, 64), (300, 3), (300, 200), (513, 128), (130, 65), (260, 256), (200, 300), (2000, 128), (1100, 37), (300, 512), (1500, 192)])
 def test_gram_tolerance(tg, orc, cuda, n, d):
     pts = orc.gen_points(n, d, 11 + d)
     _check(orc, pts, _gram(tg, cuda, pts))
