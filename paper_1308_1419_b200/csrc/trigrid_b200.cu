@@ -197,8 +197,7 @@ struct DeviceCtx {
     unsigned int* flags = nullptr;       // classify verdicts (ring, one per launch)
     unsigned flag_next = 0;
     unsigned long long* scratch = nullptr;  // [0] sink [1] bad [2] first [3] hits
-    Buf bufs[7];  // [0] pts [1] out (host drop-ins) [2] counts [3] gen [4] gram norms [5] gram operands
-                  // [6] feature-major points (d > 4 span kernel)
+    Buf bufs[4];  // [0] pts [1] out (host drop-ins) [2] counts [3] gen
     cudaEvent_t ev[34];
 };
 
@@ -216,6 +215,27 @@ tg_status ensure_buf(Buf& b, size_t bytes) {
     b.cap = 0;
     TG_CUDA(cudaMalloc(&b.p, std::max<size_t>(bytes, 256)));
     b.cap = std::max<size_t>(bytes, 256);
+    return TG_OK;
+}
+
+// Stream-ordered scratch for one launch (cudaMallocAsync from the device's
+// default pool, which keeps the memory between launches): the Gram operands and
+// the feature-major points are private to the launch, so concurrent launches
+// on other streams / host threads never share them.
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t st = nullptr;
+    Scratch() = default;
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+tg_status scratch_alloc(Scratch& s, size_t bytes, cudaStream_t st) {
+    s.st = st;
+    TG_CUDA(cudaMallocAsync(&s.p, std::max<size_t>(bytes, 256), st));
     return TG_OK;
 }
 
@@ -239,6 +259,10 @@ tg_status get_ctx(int device, DeviceCtx** out) {
         TG_CUDA(cudaMalloc(&c.flags, kFlagRing * sizeof(unsigned int)));
         TG_CUDA(cudaMalloc(&c.scratch, 256));
         for (auto& e : c.ev) TG_CUDA(cudaEventCreate(&e));
+        cudaMemPool_t pool;  // keep stream-ordered scratch cached between launches
+        TG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = ~0ull;
+        TG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         c.init.store(true, std::memory_order_release);
     }
     *out = &c;
@@ -416,8 +440,9 @@ tg_status launch_wide2_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float
     const uint64_t n = g.n;
     const uint64_t n_pad = ceil_div(n + kW2Cols, kW2Cols) * kW2Cols;  // a run's 128 columns / 16 rows stay in range
     const uint32_t d_pad = (uint32_t)ceil_div(d, kW2K) * kW2K;
-    TG_TRY(ensure_buf(c->bufs[6], (size_t)n_pad * d_pad * sizeof(float)));
-    float* ptsT = static_cast<float*>(c->bufs[6].p);
+    Scratch sp;
+    TG_TRY(scratch_alloc(sp, (size_t)n_pad * d_pad * sizeof(float), st));
+    float* ptsT = static_cast<float*>(sp.p);
     transpose_points_kernel<<<dim3((unsigned)(n_pad / 32), (unsigned)ceil_div(d_pad, 32)), dim3(32, 8), 0, st>>>(
         pts, n, d, n_pad, d_pad, ptsT);
     const size_t smem = kW2Groups * kW2GroupFloats * sizeof(float);
@@ -515,10 +540,11 @@ tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, ui
     const uint64_t a_bytes = nt * nk * (uint64_t)kG2Slice;
     const uint64_t bslice = (nt * 16 + 1) * (uint64_t)kG2Group;
     const uint64_t b_bytes = nk * 2 * bslice;
-    TG_TRY(ensure_buf(c->bufs[4], (n_pad + 8) * sizeof(float)));
-    TG_TRY(ensure_buf(c->bufs[5], a_bytes + b_bytes + 256));
-    float* norms = static_cast<float*>(c->bufs[4].p);
-    uint8_t* opA = static_cast<uint8_t*>(c->bufs[5].p);
+    Scratch sn, so;
+    TG_TRY(scratch_alloc(sn, (n_pad + 8) * sizeof(float), st));
+    TG_TRY(scratch_alloc(so, a_bytes + b_bytes + 256, st));
+    float* norms = static_cast<float*>(sn.p);
+    uint8_t* opA = static_cast<uint8_t*>(so.p);
     uint8_t* opB = opA + a_bytes;
     unsigned int* maxbits = reinterpret_cast<unsigned int*>(opB + b_bytes);
     TG_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned int), st));
@@ -918,9 +944,10 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
         if (!gram_v1()) {
             TG_TRY(launch_gram2_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out), c, st));
         } else {
-            TG_TRY(ensure_buf(c->bufs[4], n * sizeof(float)));
-            TG_TRY(launch_gram_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out),
-                                   static_cast<float*>(c->bufs[4].p), st, c->sms));
+            Scratch sn;
+            TG_TRY(scratch_alloc(sn, n * sizeof(float), st));
+            TG_TRY(launch_gram_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out), static_cast<float*>(sn.p),
+                                   st, c->sms));
         }
         TG_TRY(timer.finish(&st_local));
         if (stats) *stats = st_local;
