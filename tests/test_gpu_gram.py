@@ -75,3 +75,32 @@ def test_gram_tolerance_adversarial(tg, orc, cuda, kind):
         pts = pts - 0.5
     pts = pts.astype(np.float32)
     _check(orc, pts, _gram(tg, cuda, pts))
+
+
+def test_gram_concurrent_streams(tg, orc, cuda):
+    """Two host threads, two streams, different inputs: the per-launch device
+    scratch (operands, norms) is private, so each result equals its serial run."""
+    import threading
+
+    import torch
+    pa = torch.from_numpy(orc.gen_points(3000, 64, 1)).to(cuda)
+    pb = torch.from_numpy(orc.gen_points(3000, 100, 2)).to(cuda)
+    want_a = tg.edm(pa, mode="gram").cpu()
+    want_b = tg.edm(pb, mode="gram").cpu()
+    got = {}
+
+    def run(key, pts):
+        s = torch.cuda.Stream()
+        outs = []
+        for _ in range(4):
+            outs.append(tg.edm(pts, mode="gram", stream=s))
+        s.synchronize()
+        got[key] = [o.cpu() for o in outs]
+
+    ts = [threading.Thread(target=run, args=("a", pa)), threading.Thread(target=run, args=("b", pb))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(torch.equal(o, want_a) for o in got["a"])
+    assert all(torch.equal(o, want_b) for o in got["b"])
