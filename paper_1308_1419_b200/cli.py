@@ -107,6 +107,23 @@ def run_edm(a) -> int:
         print(f"wrote {out.numel()} packed cells to {a.out}")
     if a.check:
         ref = tg.edm(pts, strategy="ltm-exact", rho=a.rho, mode="grid")
+        if a.mode == "gram":  # stated tolerance, not bit-exact
+            nrm = (pts.double() ** 2).sum(1)
+            ok, worst = True, 0.0
+            for r0 in range(0, a.n, 1024):  # row blocks of the packed layout
+                r1 = min(a.n, r0 + 1024)
+                e0, e1 = r0 * (r0 + 1) // 2, r1 * (r1 + 1) // 2
+                i = torch.repeat_interleave(torch.arange(r0, r1, device=pts.device),
+                                            torch.arange(r0 + 1, r1 + 1, device=pts.device))
+                j = torch.arange(e0, e1, device=pts.device) - i * (i + 1) // 2
+                err = (out[e0:e1].double() ** 2 - ref[e0:e1].double() ** 2).abs()
+                ratio = err / (2.0 ** -17 * (nrm[i] + nrm[j])).clamp_min(1e-300)
+                worst = max(worst, float(ratio.max()))
+                ok = ok and bool((out[e0:e1][i == j] == 0).all())
+            ok = ok and worst <= 1.0
+            print(f"oracle check (gram tolerance |d^2 - d_exact^2| <= 2^-17 (|x_i|^2 + |x_j|^2)): "
+                  f"max err/bound = {worst:.3g} -> " + ("within tolerance" if ok else "OUT OF TOLERANCE"))
+            return 0 if ok else 1
         same = bool(torch.equal(out.view(torch.int32), ref.view(torch.int32)))
         print("oracle check: " + ("bitwise identical" if same else "MISMATCH"))
         if not same:
@@ -149,7 +166,7 @@ def main(argv=None) -> int:
     m.add_argument("--workers", default="AUTO")
     m.add_argument("--out", default="")
     m.add_argument("--check", action="store_true")
-    m.add_argument("--mode", default="auto", choices=["auto", "grid", "span"])
+    m.add_argument("--mode", default="auto", choices=["auto", "grid", "span", "gram"])
     a = p.parse_args(argv)
     try:
         return {"bench": run_bench, "verify": run_verify, "exactness": run_exactness, "edm": run_edm}[a.cmd](a)

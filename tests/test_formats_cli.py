@@ -107,6 +107,9 @@ def test_cli_gpu_commands(tg, tmp_path, orc, capsys):
     assert recs and all(r.verified == "passed" for r in recs)
     assert {r.strategy for r in recs} == {"bb", "ltm-x", "ltm-n", "ltm-r", "utm", "rb", "rec"}
     assert os.path.exists(str(csv) + ".fit.json")
+    # Gram mode: the check is the stated tolerance, reported as max err / bound
+    assert cli.main(["edm", "--n", "700", "--features", "40", "--strategy", "ltm-r", "--mode", "gram", "--check"]) == 0
+    assert "within tolerance" in capsys.readouterr().out
 
 
 @pytest.mark.gpu
