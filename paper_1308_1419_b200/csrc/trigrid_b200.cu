@@ -372,8 +372,8 @@ tg_status plan_span_c(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint
     return TG_OK;
 }
 
-uint64_t span_grid(const SpanGeom& g, bool persistent, int sms, int occ) {
-    const uint64_t need = ceil_div(g.units, kWarpsPerCta);
+uint64_t span_grid(const SpanGeom& g, bool persistent, int sms, int occ, int warps_per_cta = kWarpsPerCta) {
+    const uint64_t need = ceil_div(g.units, (uint64_t)warps_per_cta);
     if (need == 0) return 0;
     uint64_t grid = need;
     if (persistent) grid = std::min<uint64_t>(need, (uint64_t)sms * std::max(occ, 1));
@@ -392,10 +392,10 @@ template <int D, int P, bool PK>
 tg_status launch_span_edm_t(const SpanGeom& g, OutWin ow, const float* pts, float* out,
                             const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
     static int occ = -1;
-    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_edm_kernel<D, P, PK>, kWarpsPerCta * 32, 0);
-    const uint64_t grid = span_grid(g, persistent, sms, occ);
+    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_edm_kernel<D, P, PK>, kEdmWarps * 32, 0);
+    const uint64_t grid = span_grid(g, persistent, sms, occ, kEdmWarps);
     if (!grid) return TG_OK;
-    span_edm_kernel<D, P, PK><<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, ow, pts, out, flag);
+    span_edm_kernel<D, P, PK><<<(unsigned)grid, kEdmWarps * 32, 0, st>>>(g, ow, pts, out, flag);
     ++g_launches;
     TG_CUDA(cudaGetLastError());
     return TG_OK;
@@ -1069,7 +1069,8 @@ tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spher
         } else if (grid) {
             // partial words at row-segment ends are OR-ed into a zeroed table
             TG_CUDA(cudaMemsetAsync(bits, 0, ceil_div(p1 - p0, 32) * 4, st));
-            span_collide2_kernel<8><<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(
+            const uint64_t grid2 = span_grid(g, o.persistent != 0, c->sms, 32, kCollideWarps);
+            span_collide2_kernel<8><<<(unsigned)grid2, kCollideWarps * 32, 0, st>>>(
                 g, p0, reinterpret_cast<const float4*>(spheres), r_max, bits,
                 reinterpret_cast<unsigned long long*>(hits));
             ++g_launches;
