@@ -452,11 +452,11 @@ tg_status launch_wide2_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float
         attr = true;
     }
     static int occ = -1;
-    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_edm_kernel, 256, smem);
+    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_edm_kernel, kW2Threads, smem);
     const uint64_t grid =
         std::min<uint64_t>(ceil_div(g.units, kW2Groups), (uint64_t)sms * std::max(occ, 1) * (persistent ? 1 : 64));
     if (!grid) return TG_OK;
-    wide2_edm_kernel<<<(unsigned)grid, 256, smem, st>>>(g, ow, ptsT, n_pad, d_pad / kW2K, out, flag);
+    wide2_edm_kernel<<<(unsigned)grid, kW2Threads, smem, st>>>(g, ow, ptsT, n_pad, d_pad / kW2K, out, flag);
     g_launches += 2;
     TG_CUDA(cudaGetLastError());
     return TG_OK;
