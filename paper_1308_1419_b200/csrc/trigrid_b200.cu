@@ -1058,7 +1058,7 @@ tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spher
         SpanGeom g;
         // v2: runs of up to 256 columns (8 column slots per lane)
         TG_TRY(plan_span(s, n, rho, rows[o.shard_index], rows[o.shard_index + 1],
-                         std::max<uint32_t>(1, (collide_v1() ? 128 : 256) / rho), &g));
+                         std::max<uint32_t>(1, (collide_v1() ? 128 : 32 * TG_COLLIDE_SLOTS) / rho), &g));
         const uint64_t grid = span_grid(g, o.persistent != 0, c->sms, 8);
         if (grid && collide_v1()) {
             span_collide_kernel<<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(
@@ -1070,7 +1070,7 @@ tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spher
             // partial words at row-segment ends are OR-ed into a zeroed table
             TG_CUDA(cudaMemsetAsync(bits, 0, ceil_div(p1 - p0, 32) * 4, st));
             const uint64_t grid2 = span_grid(g, o.persistent != 0, c->sms, 32, kCollideWarps);
-            span_collide2_kernel<8><<<(unsigned)grid2, kCollideWarps * 32, 0, st>>>(
+            span_collide2_kernel<TG_COLLIDE_SLOTS><<<(unsigned)grid2, kCollideWarps * 32, 0, st>>>(
                 g, p0, reinterpret_cast<const float4*>(spheres), r_max, bits,
                 reinterpret_cast<unsigned long long*>(hits));
             ++g_launches;
