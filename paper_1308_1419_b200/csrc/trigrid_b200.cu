@@ -196,12 +196,19 @@ struct DeviceCtx {
     cudaStream_t copy_stream2 = nullptr; // second D2H stream (alternating 256 MB sub-copies)
     unsigned int* flags = nullptr;       // classify verdicts (ring, one per launch)
     unsigned flag_next = 0;
+    unsigned long long* queues = nullptr;  // persistent-launch unit counters (ring, one per launch)
+    unsigned queue_next = 0;
     unsigned long long* scratch = nullptr;  // [0] sink [1] bad [2] first [3] hits
     Buf bufs[4];  // [0] pts [1] out (host drop-ins) [2] counts [3] gen
     cudaEvent_t ev[34];
 };
 
 DeviceCtx g_ctx[64];
+
+unsigned long long* next_queue_for(DeviceCtx* c) {
+    const unsigned slot = __atomic_fetch_add(&c->queue_next, 1u, __ATOMIC_RELAXED) % kFlagRing;
+    return c->queues + slot;
+}
 
 unsigned int* next_flag(DeviceCtx* c) {
     const unsigned slot = __atomic_fetch_add(&c->flag_next, 1u, __ATOMIC_RELAXED) % kFlagRing;
@@ -257,6 +264,7 @@ tg_status get_ctx(int device, DeviceCtx** out) {
         TG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
         TG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream2, cudaStreamNonBlocking));
         TG_CUDA(cudaMalloc(&c.flags, kFlagRing * sizeof(unsigned int)));
+        TG_CUDA(cudaMalloc(&c.queues, kFlagRing * sizeof(unsigned long long)));
         TG_CUDA(cudaMalloc(&c.scratch, 256));
         for (auto& e : c.ev) TG_CUDA(cudaEventCreate(&e));
         cudaMemPool_t pool;  // keep stream-ordered scratch cached between launches
@@ -395,7 +403,14 @@ tg_status launch_span_edm_t(const SpanGeom& g, OutWin ow, const float* pts, floa
     if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_edm_kernel<D, P, PK>, kEdmWarps * 32, 0);
     const uint64_t grid = span_grid(g, persistent, sms, occ, kEdmWarps);
     if (!grid) return TG_OK;
-    span_edm_kernel<D, P, PK><<<(unsigned)grid, kEdmWarps * 32, 0, st>>>(g, ow, pts, out, flag);
+    unsigned long long* queue = nullptr;
+    if (persistent) {  // dynamic unit queue: a per-launch zeroed counter
+        DeviceCtx* c;
+        TG_TRY(get_ctx(-1, &c));  // the current device (the launch already initialised it)
+        queue = next_queue_for(c);
+        TG_CUDA(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
+    }
+    span_edm_kernel<D, P, PK><<<(unsigned)grid, kEdmWarps * 32, 0, st>>>(g, ow, pts, out, flag, queue);
     ++g_launches;
     TG_CUDA(cudaGetLastError());
     return TG_OK;
