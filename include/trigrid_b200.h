@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define TG_API_VERSION 1
+#define TG_API_VERSION 2
 
 typedef enum {
     TG_OK = 0,
@@ -59,12 +59,15 @@ typedef enum {
     TG_KERNEL_DUMMY = 0, /* launch_dummy  engine.cpp:150-155: mapping cost only */
     TG_KERNEL_WRITE = 1, /* packed u32 i+j (the dummy kernel made HBM-visible)  */
     TG_KERNEL_EDM = 2,   /* launch_edm    engine.cpp:157-175: packed fp32 EDM   */
-    TG_KERNEL_COUNT = 3  /* launch_count  engine.cpp:177-188: u32 += 1 per cell */
+    TG_KERNEL_COUNT = 3  /* launch_count  engine.cpp:177-188: u32 += 1 per cell (span: per cell of
+                            every owned 16-byte chunk -- the exactly-once check of the span rule) */
 } tg_kernel;
 
 /* Execution mode. */
 typedef enum {
-    TG_MODE_AUTO = 0, /* span for bb/ltm/rec when rho % 4 == 0 and the body allows (edm, write), else grid */
+    TG_MODE_AUTO = 0, /* span when the strategy/rho/body allow it (bb, ltm-*, rec, rb: rho % 4 == 0;
+                         utm: rho a power of two in [4, 128]; bodies edm d <= 4, write, count;
+                         d > 4 and collide: bb, ltm-*, rec), else grid */
     TG_MODE_GRID = 1, /* paper-faithful: one CTA of rho*rho threads per grid block, one cell per thread */
     TG_MODE_SPAN = 2, /* B200: warp per run of consecutive blocks, 128-bit owned-chunk stores */
     TG_MODE_GRAM = 3  /* EDM only: Gram trick on tcgen05 (fp16 hi/lo split, kind::f16, any d),
@@ -92,7 +95,31 @@ typedef struct {
     uint32_t shard_count;  /* 0 or 1 = whole domain */
     uint64_t sentinel;     /* dummy kernel: runtime value i+j is compared with (never matches) */
     void* sink;            /* dummy kernel: optional device u64 sink (else internal) */
+    /* ---- API version 2 */
+    uint64_t rec_m;        /* REC schedule N = m * 2^k (rec_schedule, strategies.cpp:116-140);
+                              0 = the largest-k decomposition of make_strategy (rec_decompose) */
+    uint32_t rec_k;
+    int32_t engine;        /* UTM sqrt engine (StrategyId{UpperTri, engine}, strategies.hpp:27-31):
+                              0 native, 1 newton, 2 reciprocal, 3 exact; -1 = newton (parse_strategy("utm")) */
+    tg_dispatch_stats* per_pass;  /* LaunchOptions::per_pass (engine.hpp:36, engine.cpp:87-133): when
+                                     non-NULL, one entry per grid pass (tg_grid_spec order), each pass
+                                     launched and device-timed on its own */
+    uint32_t per_pass_cap;        /* entries available at per_pass */
+    uint32_t n_devices;           /* host drop-ins: 0/1 = `device` only; > 1 = split the lambda range
+                                     into n_devices shards, one per devices[g], each copying its
+                                     packed slice out over its own PCIe link */
+    const int32_t* devices;
 } tg_launch_opts;
+
+/* One grid pass (trigrid::Pass + RecLevel, strategies.hpp:40-60). */
+typedef struct {
+    uint64_t blocks_x;
+    uint64_t blocks_y;
+    uint32_t has_level;  /* REC passes carry a level tag */
+    uint32_t level;      /* 0 = diagonal pass */
+    uint64_t side;
+    uint64_t squares;
+} tg_pass;
 
 void tg_launch_opts_init(tg_launch_opts* o);
 
@@ -130,10 +157,24 @@ tg_status tg_improvement_model(double beta, double tau, double n, double* out);
 /* Strategy name <-> id (parse_strategy strategies.cpp:19-28 + "ltm-exact"). */
 tg_status tg_parse_strategy(const char* name, tg_strategy* out);
 
+/* grid_of / rec_schedule / rb_grid (strategies.hpp:393-400, strategies.cpp:107-140): the
+ * strategy's grid passes.  opts supplies rec_m/rec_k (may be NULL).  *npass is set even when
+ * cap is too small (then TG_EINVAL). */
+tg_status tg_grid_spec(tg_strategy s, uint64_t n, uint32_t rho, const tg_launch_opts* opts, tg_pass* passes,
+                       uint32_t cap, uint32_t* npass);
+
+/* ltm_map with the reference's RepairPolicy (strategies.cpp:60-83, fastmath.hpp:84-103):
+ * repair 0 = Auto (repair for lambda >= 1,844,160), 1 = Off (float row only), 2 = On.
+ * Host binary32 arithmetic identical to the reference (engine 2 = 1/sqrtf). */
+tg_status tg_ltm_map_policy(uint64_t lambda, int engine, int with_diag, int repair, uint64_t* i, uint64_t* j);
+
 /* Closed-form DispatchStats of a launch (what run_strategy tallies,
  * engine.cpp:70-136) for the whole domain or one shard. */
 tg_status tg_dispatch_stats_for(tg_strategy s, uint64_t n, uint32_t rho, uint32_t shard_index,
                                 uint32_t shard_count, tg_dispatch_stats* out);
+/* Same with a full option set (rec_m/rec_k, shard); per-pass stats into opts->per_pass when set. */
+tg_status tg_dispatch_stats_opts(tg_strategy s, uint64_t n, uint32_t rho, const tg_launch_opts* opts,
+                                 tg_dispatch_stats* out);
 
 /* Lambda-range sharding across G devices (new): block-row bounds
  * rows[0..G] with rows[0] = 0, rows[G] = ceil(N/rho); shard g owns block rows
@@ -151,7 +192,7 @@ tg_status tg_shard_elems(uint64_t n, uint32_t rho, uint32_t shard_index, uint32_
  *   pts : device float[N*d] row-major (EDM only; 16-byte aligned), d >= 1
  *   out : EDM   -> device float[shard elems]  (packed lambda order, engine.hpp:62-64)
  *         WRITE -> device uint32[shard elems] (i+j)
- *         COUNT -> device uint32[T(N)], incremented (caller zeroes)
+ *         COUNT -> device uint32[shard elems] (T(N) unsharded), incremented (caller zeroes)
  *         DUMMY -> ignored (see opts->sink)
  * Unlike the reference, EDM accepts any d >= 1 (the reference caps d at 4,
  * engine.cpp:162-163); d in {1,2,3,4} use the register-window span kernel. */
@@ -182,6 +223,28 @@ tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint
  * (checks.cpp:16-38): 1 when every domain cell is touched exactly once
  * (no-diagonal domain for utm), computed with the COUNT kernel on device. */
 tg_status tg_coverage_ok(tg_strategy s, uint64_t n, uint32_t rho, int device, int* ok);
+/* Same with options: mode (AUTO = the kernel shape EDM/write launches use, SPAN checks the
+ * owned-chunk rule of the span kernels, GRID the paper-faithful kernel), rec_m/rec_k, engine;
+ * bad (may be NULL) = number of wrong cells, first_bad (may be NULL) = first wrong element. */
+tg_status tg_coverage_ok_opts(tg_strategy s, uint64_t n, uint32_t rho, const tg_launch_opts* opts, int* ok,
+                              uint64_t* bad, uint64_t* first_bad);
+
+/* launch_count (engine.cpp:177-188) with the reference's HOST counter vector: counts (host
+ * uint32[T(N)]) are incremented in place by the COUNT kernel on device. */
+tg_status tg_count_host(tg_strategy s, uint64_t n, uint32_t rho, uint32_t* counts, const tg_launch_opts* opts,
+                        tg_dispatch_stats* stats);
+
+/* launch_dummy (engine.cpp:150-155) from the host: the dummy kernel on device, synchronous;
+ * *sink_value = the device sink's value after the launch (the anti-DCE store never fires for
+ * the default sentinel, so it stays as it was: 0). */
+tg_status tg_dummy_host(tg_strategy s, uint64_t n, uint32_t rho, const tg_launch_opts* opts,
+                        tg_dispatch_stats* stats, uint64_t* sink_value);
+
+/* edm_reference (edm.cpp:53-63): the reference API's SEQUENTIAL oracle, i.e. host code by
+ * contract (every pair j <= i in row-major order, binary32 edm_pair arithmetic, any d).  It is
+ * what launch_edm results are verified against (run_suite, bench.cpp:80-108) -- never a
+ * fallback for the device path. */
+tg_status tg_edm_reference_host(const float* pts, uint64_t n, uint32_t d, float* out);
 
 /* ltm_exactness_sweep (checks.cpp:81-95) generalised: on device, for every
  * lambda in [begin, end) compare the g(lambda) row (float guess only when

@@ -31,7 +31,22 @@ class tg_dispatch_stats(C.Structure):
 class tg_launch_opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("mode", C.c_uint32), ("stream", C.c_void_p),
                 ("async_", C.c_uint32), ("persistent", C.c_uint32), ("shard_index", C.c_uint32),
-                ("shard_count", C.c_uint32), ("sentinel", C.c_uint64), ("sink", C.c_void_p)]
+                ("shard_count", C.c_uint32), ("sentinel", C.c_uint64), ("sink", C.c_void_p),
+                # API version 2
+                ("rec_m", C.c_uint64), ("rec_k", C.c_uint32), ("engine", C.c_int32),
+                ("per_pass", C.POINTER(tg_dispatch_stats)), ("per_pass_cap", C.c_uint32),
+                ("n_devices", C.c_uint32), ("devices", C.POINTER(C.c_int32))]
+
+
+class tg_pass(C.Structure):
+    _fields_ = [("blocks_x", C.c_uint64), ("blocks_y", C.c_uint64), ("has_level", C.c_uint32),
+                ("level", C.c_uint32), ("side", C.c_uint64), ("squares", C.c_uint64)]
+
+    def as_dict(self) -> dict:
+        d = {"blocks_x": int(self.blocks_x), "blocks_y": int(self.blocks_y)}
+        if self.has_level:
+            d["level"] = {"level": int(self.level), "side": int(self.side), "squares": int(self.squares)}
+        return d
 
 
 _u64, _u32, _i32 = C.c_uint64, C.c_uint32, C.c_int
@@ -72,6 +87,14 @@ _SIGS = {
     "tg_sqrt_selftest": (_st, [_u32, _u32, C.c_int, _pu64]),
     "tg_gen_values": (_st, [_u64, _u64, C.c_void_p, _popts]),
     "tg_gen_points_host": (_st, [_u64, _u32, _u64, C.c_void_p, C.c_int]),
+    # API version 2
+    "tg_grid_spec": (_st, [C.c_int, _u64, _u32, _popts, C.POINTER(tg_pass), _u32, C.POINTER(C.c_uint32)]),
+    "tg_ltm_map_policy": (_st, [_u64, C.c_int, C.c_int, C.c_int, _pu64, _pu64]),
+    "tg_dispatch_stats_opts": (_st, [C.c_int, _u64, _u32, _popts, _pstats]),
+    "tg_coverage_ok_opts": (_st, [C.c_int, _u64, _u32, _popts, C.POINTER(C.c_int), _pu64, _pu64]),
+    "tg_count_host": (_st, [C.c_int, _u64, _u32, C.c_void_p, _popts, _pstats]),
+    "tg_dummy_host": (_st, [C.c_int, _u64, _u32, _popts, _pstats, _pu64]),
+    "tg_edm_reference_host": (_st, [C.c_void_p, _u64, _u32, C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -117,9 +140,22 @@ def check(status: int) -> None:
 
 def opts(device: int = -1, mode: str = "auto", stream: int | None = None, async_: bool = False,
          persistent: bool = False, shard: tuple[int, int] | None = None, sentinel: int | None = None,
-         sink: int | None = None) -> tg_launch_opts:
+         sink: int | None = None, rec: tuple[int, int] | None = None, engine: int | None = None,
+         per_pass=None, devices=None) -> tg_launch_opts:
+    """Build a tg_launch_opts.  per_pass: a ctypes array of tg_dispatch_stats;
+    devices: a ctypes c_int32 array (kept alive by the caller)."""
     o = tg_launch_opts()
     load().tg_launch_opts_init(C.byref(o))
+    if rec is not None:
+        o.rec_m, o.rec_k = int(rec[0]), int(rec[1])
+    if engine is not None:
+        o.engine = int(engine)
+    if per_pass is not None:
+        o.per_pass = C.cast(per_pass, C.POINTER(tg_dispatch_stats))
+        o.per_pass_cap = len(per_pass)
+    if devices is not None:
+        o.devices = C.cast(devices, C.POINTER(C.c_int32))
+        o.n_devices = len(devices)
     o.device = device
     o.mode = MODES[mode]
     o.stream = stream or None

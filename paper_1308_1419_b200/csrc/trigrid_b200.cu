@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/trigrid_b200.h"
@@ -59,20 +60,49 @@ int ltm_engine(tg_strategy s) {
     }
 }
 
+// A strategy instance: make_strategy(StrategyId, ProblemSize) (strategies.cpp:
+// 192-208) plus the RecStrategy schedule (m, k) a caller may pick
+// (rec_schedule, strategies.cpp:116-140) and the UTM engine.
+struct Problem {
+    tg_strategy s;
+    uint64_t n;
+    uint32_t rho;
+    uint64_t m = 0;  // REC
+    uint32_t k = 0;
+    int engine = kNewton;  // UTM (parse_strategy("utm"), strategies.cpp:24)
+};
+
 // ProblemSize (tri.cpp:9-15) plus the per-strategy constructors' checks.
-tg_status validate_problem(tg_strategy s, uint64_t n, uint32_t rho) {
+tg_status make_problem(tg_strategy s, uint64_t n, uint32_t rho, const tg_launch_opts* o, Problem* P) {
     if (n == 0) return fail(TG_EINVAL, "ProblemSize: N must be >= 1");
     if (n > kMaxElems) return fail(TG_EINVAL, "ProblemSize: N exceeds the 2^20 cap");
     if (rho == 0) return fail(TG_EINVAL, "ProblemSize: rho must be >= 1");
     if ((int)s < 0 || (int)s > (int)TG_REC) return fail(TG_EINVAL, "make_strategy: unknown strategy kind");
     if (s == TG_RB && n < 2) return fail(TG_EINVAL, "rb_rect: N must be >= 2");
+    *P = Problem{s, n, rho};
+    if (s == TG_UTM && o && o->engine >= 0) {
+        if (o->engine > 3) return fail(TG_EINVAL, "make_strategy: unknown sqrt engine");
+        P->engine = o->engine;
+    }
     if (s == TG_REC) {
-        uint64_t m;
-        uint32_t k;
-        if (!rec_decompose(n, rho, &m, &k))
+        if (o && (o->rec_m || o->rec_k)) {  // rec_schedule's own checks (strategies.cpp:118-124)
+            if (o->rec_k < 1 || o->rec_k > 40) return fail(TG_EINVAL, "rec_schedule: k must be in [1, 40]");
+            if (o->rec_m == 0 || o->rec_m % rho != 0)
+                return fail(TG_EINVAL, "rec_schedule: m must be a positive multiple of rho");
+            if (o->rec_m > (kMaxElems >> 1) || n != (o->rec_m << o->rec_k))
+                return fail(TG_EINVAL, "rec_schedule: N must equal m*2^k");
+            P->m = o->rec_m;
+            P->k = o->rec_k;
+        } else if (!rec_decompose(n, rho, &P->m, &P->k)) {
             return fail(TG_EINVAL, "rec: N is not m*2^k with m a multiple of rho");
+        }
     }
     return TG_OK;
+}
+
+tg_status validate_problem(tg_strategy s, uint64_t n, uint32_t rho) {
+    Problem P;
+    return make_problem(s, n, rho, nullptr, &P);
 }
 
 // ------------------------------------------------------------ sharding
@@ -114,23 +144,82 @@ uint64_t tile_threads_discarded(uint64_t n, uint64_t rho, uint64_t b0, uint64_t 
     return t;
 }
 
-struct RecPlan {
-    uint64_t m;
-    uint32_t k;
+// Block-row window of shard `shard` of G: block rows [b0, b1), cell rows [r_lo, r_hi).
+struct Window {
+    uint64_t b0, b1, r_lo, r_hi;
 };
+Window window_of(const Problem& P, uint32_t shard, uint32_t G) {
+    const auto rows = shard_rows(ceil_div(P.n, P.rho), G);
+    Window w{rows[shard], rows[shard + 1], 0, 0};
+    w.r_lo = std::min<uint64_t>(P.n, w.b0 * P.rho);
+    w.r_hi = std::min<uint64_t>(P.n, w.b1 * P.rho);
+    return w;
+}
 
-tg_status stats_for(tg_strategy s, uint64_t n, uint32_t rho, uint32_t shard, uint32_t shards,
-                    tg_dispatch_stats* st) {
-    TG_TRY(validate_problem(s, n, rho));
+// REC grid passes in the reference's order (rec_schedule, strategies.cpp:
+// 116-140): levels 1..k (square side m 2^(l-1), 2^(k-l) squares), then the
+// diagonal pass (level 0: 2^k triangles of side m).
+struct RecPassInfo {
+    uint32_t level;
+    uint64_t side, sb, count;  // count = squares or triangles
+};
+std::vector<RecPassInfo> rec_passes(const Problem& P) {
+    std::vector<RecPassInfo> v;
+    for (uint32_t level = 1; level <= P.k; ++level) {
+        const uint64_t side = P.m << (level - 1);
+        v.push_back({level, side, side / P.rho, 1ull << (P.k - level)});
+    }
+    v.push_back({0, P.m, P.m / P.rho, 1ull << P.k});
+    return v;
+}
+
+// Global block row of pass-local block row `by` (strictly increasing in by).
+uint64_t rec_row_of(const RecPassInfo& q, uint64_t by) {
+    if (q.level == 0) return by;  // triangle t at block row t sb
+    const uint64_t sq = by / q.sb, ly = by % q.sb;
+    return (2 * sq + 1) * q.sb + ly;  // rec_block_map (strategies.hpp:214-220)
+}
+// First pass-local block row whose global row is >= X.
+uint64_t rec_row_lower_bound(const RecPassInfo& q, uint64_t X) {
+    uint64_t lo = 0, hi = q.sb * q.count;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (rec_row_of(q, mid) >= X) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+// RB rect block rows whose direct (level 0) / folded (level 1) part meets cell rows [r_lo, r_hi).
+void rb_row_ranges(const Problem& P, const Window& w, uint64_t* y) {
+    const uint64_t n = P.n, rho = P.rho, even = (n % 2 == 0);
+    const uint64_t h = even ? n + 1 : n, hb = ceil_div(h, rho);
+    if (w.r_hi <= w.r_lo) {
+        y[0] = y[1] = y[2] = y[3] = 0;
+        return;
+    }
+    // direct part: row i = ty - even
+    y[0] = std::min(hb, (w.r_lo + even) / rho);
+    y[1] = std::min(hb, ceil_div(w.r_hi + even, rho));
+    // folded part: row i = n - 1 - ty, ty in [n - r_hi, n - r_lo)
+    y[2] = std::min(hb, (n - w.r_hi) / rho);
+    y[3] = std::min(hb, ceil_div(n - w.r_lo, rho));
+}
+
+// What run_strategy tallies (engine.cpp:70-136), closed form, for the whole
+// domain or one shard; per_pass (optional) gets one entry per grid pass.
+tg_status stats_for(const Problem& P, uint32_t shard, uint32_t shards, tg_dispatch_stats* st,
+                    std::vector<tg_dispatch_stats>* per_pass = nullptr) {
+    const uint64_t n = P.n, rho = P.rho;
     *st = tg_dispatch_stats{0, 0, 0, 0};
+    if (per_pass) per_pass->clear();
     const uint64_t nb = ceil_div(n, rho);
     const uint32_t G = shards == 0 ? 1 : shards;
     if (shard >= G) return fail(TG_EINVAL, "shard_index must be < shard_count");
-    if (G > 1 && !(s == TG_BB || is_ltm(s)))
-        return fail(TG_EINVAL, "lambda-range sharding applies to bb and ltm-* only");
+    const Window w = window_of(P, shard, G);
+    const tg_strategy s = P.s;
     if (s == TG_BB || is_ltm(s)) {
-        const auto rows = shard_rows(nb, G);
-        const uint64_t b0 = rows[shard], b1 = rows[shard + 1];
+        const uint64_t b0 = w.b0, b1 = w.b1;
         if (s == TG_BB) {
             const uint64_t W = b1, H = b1 - b0;
             st->blocks_launched = W * H;
@@ -143,42 +232,56 @@ tg_status stats_for(tg_strategy s, uint64_t n, uint32_t rho, uint32_t shard, uin
             st->blocks_discarded = side * side - L;
         }
         st->threads_discarded = (b1 > b0) ? tile_threads_discarded(n, rho, b0, b1) : 0;
+    } else if (s == TG_UTM) {
+        if (G == 1) {
+            const uint64_t pairs = tri_nd(n), tpb = rho * rho;
+            const uint64_t blocks = pairs == 0 ? 1 : ceil_div(pairs, tpb);
+            st->blocks_launched = blocks;
+            st->threads_discarded = blocks * tpb - pairs;
+        } else {  // shard: the rho x rho tiles of its rows the span walk visits (no reference counterpart)
+            const uint64_t H = w.b1 - w.b0;
+            st->blocks_launched = w.b0 * H + tri(H);
+        }
+    } else if (s == TG_RB) {
+        const uint64_t wd = (n % 2 == 0) ? n / 2 : (n + 1) / 2, h = (n % 2 == 0) ? n + 1 : n;
+        const uint64_t gx = ceil_div(wd, rho), gy = ceil_div(h, rho);
+        if (G == 1) {
+            st->blocks_launched = gx * gy;
+            st->threads_discarded = gx * gy * rho * rho - wd * h;
+        } else {  // shard: rect blocks whose direct or folded part meets its rows
+            uint64_t y[4];
+            rb_row_ranges(P, w, y);
+            const uint64_t lo = std::max(y[0], y[2]), hi = std::min(y[1], y[3]);
+            st->blocks_launched = gx * ((y[1] - y[0]) + (y[3] - y[2]) - (hi > lo ? hi - lo : 0));
+        }
+    } else {  // REC: per pass, the pass-local block rows inside the window
+        for (const RecPassInfo& q : rec_passes(P)) {
+            const uint64_t y0 = rec_row_lower_bound(q, w.b0), y1 = rec_row_lower_bound(q, w.b1);
+            tg_dispatch_stats ps{(y1 - y0) * q.sb, 0, 0, 0};
+            if (q.level == 0) {  // diagonal pass: BB inside each m-triangle
+                for (uint64_t by = y0; by < y1; ++by) ps.blocks_discarded += q.sb - 1 - by % q.sb;
+                ps.threads_discarded = (y1 - y0) * (rho * (rho - 1) / 2);
+            }
+            st->blocks_launched += ps.blocks_launched;
+            st->blocks_discarded += ps.blocks_discarded;
+            st->threads_discarded += ps.threads_discarded;
+            if (per_pass) per_pass->push_back(ps);
+        }
         return TG_OK;
     }
-    if (s == TG_UTM) {
-        const uint64_t pairs = tri_nd(n), tpb = (uint64_t)rho * rho;
-        const uint64_t blocks = pairs == 0 ? 1 : ceil_div(pairs, tpb);
-        st->blocks_launched = blocks;
-        st->threads_discarded = blocks * tpb - pairs;
-        return TG_OK;
-    }
-    if (s == TG_RB) {
-        const uint64_t w = (n % 2 == 0) ? n / 2 : (n + 1) / 2, h = (n % 2 == 0) ? n + 1 : n;
-        const uint64_t gx = ceil_div(w, rho), gy = ceil_div(h, rho);
-        st->blocks_launched = gx * gy;
-        st->threads_discarded = gx * gy * rho * rho - w * h;
-        return TG_OK;
-    }
-    // REC
-    uint64_t m;
-    uint32_t k;
-    rec_decompose(n, rho, &m, &k);
-    uint64_t launched = 0;
-    for (uint32_t level = 1; level <= k; ++level) {
-        const uint64_t side = m << (level - 1), sb = side / rho;
-        launched += sb * sb * (1ull << (k - level));
-    }
-    const uint64_t sb = m / rho, tris = 1ull << k;
-    launched += sb * sb * tris;
-    st->blocks_launched = launched;
-    st->blocks_discarded = tris * (sb * (sb - 1) / 2);
-    st->threads_discarded = tris * sb * ((uint64_t)rho * (rho - 1) / 2);
+    if (per_pass) per_pass->push_back(*st);
+    (void)nb;
     return TG_OK;
 }
 
-// ------------------------------------------------------- device context
+tg_status stats_for(tg_strategy s, uint64_t n, uint32_t rho, uint32_t shard, uint32_t shards,
+                    tg_dispatch_stats* st) {
+    Problem P;
+    TG_TRY(make_problem(s, n, rho, nullptr, &P));
+    return stats_for(P, shard, shards, st);
+}
 
-constexpr unsigned kFlagRing = 1024;
+// ------------------------------------------------------- device context
 
 struct Buf {
     void* p = nullptr;
@@ -187,32 +290,46 @@ struct Buf {
 
 struct DeviceCtx {
     std::mutex mu;       // guards the cached buffers / internal streams of the host drop-ins
-    std::mutex init_mu;  // one-time initialisation
+    std::mutex init_mu;  // one-time initialisation (and the per-device kernel attributes below)
     std::atomic<bool> init{false};
     int dev = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;       // internal compute stream (host drop-ins)
     cudaStream_t copy_stream = nullptr;  // D2H pipeline
     cudaStream_t copy_stream2 = nullptr; // second D2H stream (alternating 256 MB sub-copies)
-    unsigned int* flags = nullptr;       // classify verdicts (ring, one per launch)
-    unsigned flag_next = 0;
-    unsigned long long* queues = nullptr;  // persistent-launch unit counters (ring, one per launch)
-    unsigned queue_next = 0;
-    unsigned long long* scratch = nullptr;  // [0] sink [1] bad [2] first [3] hits
+    unsigned long long* scratch = nullptr;  // [0] sink [1] bad [2] first [3] hits (host drop-ins, under mu)
     Buf bufs[4];  // [0] pts [1] out (host drop-ins) [2] counts [3] gen
     cudaEvent_t ev[34];
+    // per-device kernel attributes / occupancies (function attributes are per device)
+    std::atomic<bool> attr_wide2{false}, attr_gram{false}, attr_gram2{false};
+    std::atomic<int> occ_wide2{-1}, occ_edm{-1}, occ_write{-1};
 };
 
 DeviceCtx g_ctx[64];
 
-unsigned long long* next_queue_for(DeviceCtx* c) {
-    const unsigned slot = __atomic_fetch_add(&c->queue_next, 1u, __ATOMIC_RELAXED) % kFlagRing;
-    return c->queues + slot;
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per device and kernel.
+template <class K>
+tg_status ensure_smem_attr(DeviceCtx* c, std::atomic<bool>& done, K* kernel, size_t bytes) {
+    if (done.load(std::memory_order_acquire)) return TG_OK;
+    std::lock_guard<std::mutex> lk(c->init_mu);
+    if (!done.load(std::memory_order_relaxed)) {
+        TG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        done.store(true, std::memory_order_release);
+    }
+    return TG_OK;
 }
 
-unsigned int* next_flag(DeviceCtx* c) {
-    const unsigned slot = __atomic_fetch_add(&c->flag_next, 1u, __ATOMIC_RELAXED) % kFlagRing;
-    return c->flags + slot;
+template <class K>
+int occupancy(std::atomic<int>& slot, K* kernel, int threads, size_t smem) {
+    int v = slot.load(std::memory_order_relaxed);
+    if (v < 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, threads, smem) != cudaSuccess) {
+            (void)cudaGetLastError();
+            v = 1;
+        }
+        slot.store(std::max(v, 1), std::memory_order_relaxed);
+    }
+    return std::max(v, 1);
 }
 
 tg_status ensure_buf(Buf& b, size_t bytes) {
@@ -226,9 +343,10 @@ tg_status ensure_buf(Buf& b, size_t bytes) {
 }
 
 // Stream-ordered scratch for one launch (cudaMallocAsync from the device's
-// default pool, which keeps the memory between launches): the Gram operands and
-// the feature-major points are private to the launch, so concurrent launches
-// on other streams / host threads never share them.
+// default pool, which keeps the memory between launches): the Gram operands,
+// the feature-major points, the classify verdict and the persistent unit
+// counter are private to the launch, so concurrent launches on other streams
+// / host threads never share them.
 struct Scratch {
     void* p = nullptr;
     cudaStream_t st = nullptr;
@@ -245,6 +363,21 @@ tg_status scratch_alloc(Scratch& s, size_t bytes, cudaStream_t st) {
     TG_CUDA(cudaMallocAsync(&s.p, std::max<size_t>(bytes, 256), st));
     return TG_OK;
 }
+
+// Restores the caller's current device when an entry point returns (get_ctx
+// switches to the launch's device).
+struct DevGuard {
+    int prev = -1;
+    DevGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            (void)cudaGetLastError();
+            prev = -1;
+        }
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 tg_status get_ctx(int device, DeviceCtx** out) {
     int dev = device;
@@ -263,8 +396,6 @@ tg_status get_ctx(int device, DeviceCtx** out) {
         TG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         TG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
         TG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream2, cudaStreamNonBlocking));
-        TG_CUDA(cudaMalloc(&c.flags, kFlagRing * sizeof(unsigned int)));
-        TG_CUDA(cudaMalloc(&c.queues, kFlagRing * sizeof(unsigned long long)));
         TG_CUDA(cudaMalloc(&c.scratch, 256));
         for (auto& e : c.ev) TG_CUDA(cudaEventCreate(&e));
         cudaMemPool_t pool;  // keep stream-ordered scratch cached between launches
@@ -290,12 +421,28 @@ int span_slots() {
     return p;
 }
 
+bool pow2(uint64_t v) { return v && !(v & (v - 1)); }
+
+// Strategies / rho with a span form: row tiles for bb, ltm-*, rec, rb
+// (rho % 4 == 0); column runs for utm (rho / 4 must divide 32).
 bool span_eligible(tg_strategy s, uint32_t rho) {
-    return (s == TG_BB || is_ltm(s) || s == TG_REC) && rho % 4 == 0 && rho <= 128;
+    if (s == TG_UTM) return pow2(rho) && rho >= 4 && rho <= 128;
+    return (s == TG_BB || is_ltm(s) || s == TG_REC || s == TG_RB) && rho % 4 == 0 && rho <= 128;
+}
+// Bodies restricted to the square-tile strategies (16-row tiles at block-row
+// multiples: the d > 4 kernels, the collision kernel).
+bool square_tiles(tg_strategy s) { return s == TG_BB || is_ltm(s) || s == TG_REC; }
+
+// UTM grid blocks per unit (column run of C rho-row blocks).  A/B: TG_UTM_C.
+uint32_t utm_blocks_per_unit() {
+    static uint32_t v = [] {
+        const char* e = std::getenv("TG_UTM_C");
+        return e ? (uint32_t)std::max(1, std::atoi(e)) : 8u;
+    }();
+    return v;
 }
 
-tg_status plan_span_c(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64_t b1, uint32_t C,
-                      SpanGeom* g);
+tg_status plan_span_c(const Problem& P, const Window& w, uint32_t C, SpanGeom* g, int only_pass);
 
 // Units a launch should have at least: ~32 warps' worth per SM.  A small
 // problem planned with the default C (16 blocks per warp) leaves most SMs idle
@@ -309,27 +456,43 @@ uint64_t min_span_units() {  // A/B: TG_SPAN_MIN_UNITS
     return v;
 }
 
-// Geometry for block rows [b0, b1); `adaptive` lets C shrink for small problems
-// (the one-CTA-per-run d > 4 kernel needs the fixed C).
-tg_status plan_span(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64_t b1, uint32_t C,
-                    SpanGeom* g, bool adaptive = true) {
-    TG_TRY(plan_span_c(s, n, rho, b0, b1, C, g));
+// Geometry for the window's block rows; `adaptive` lets C shrink for small
+// problems (the one-CTA-per-run d > 4 kernel needs the fixed C).  only_pass
+// (REC, >= 0): plan that grid pass alone (LaunchOptions::per_pass timing).
+tg_status plan_span(const Problem& P, const Window& w, uint32_t C, SpanGeom* g, bool adaptive = true,
+                    int only_pass = -1) {
+    TG_TRY(plan_span_c(P, w, C, g, only_pass));
     const uint64_t min_units = min_span_units();
     if (!adaptive || C <= 1 || g->units >= min_units) return TG_OK;
     const uint64_t blocks = g->units * C;  // upper bound of the launch's grid blocks
     const uint32_t c2 = (uint32_t)std::max<uint64_t>(1, blocks / min_units);
-    return c2 < C ? plan_span_c(s, n, rho, b0, b1, c2, g) : TG_OK;
+    return c2 < C ? plan_span_c(P, w, c2, g, only_pass) : TG_OK;
 }
 
-tg_status plan_span_c(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint64_t b1, uint32_t C,
-                      SpanGeom* g) {
+void add_pass(SpanGeom* g, uint64_t& unit, uint64_t y0, uint64_t y1, uint64_t sb, uint64_t side, uint32_t level,
+              uint32_t C) {
+    SpanPass& q = g->pass[g->npass++];
+    q.unit_begin = unit;
+    q.y0 = y0;
+    q.sb = sb;
+    q.side = side;
+    q.level = level;
+    q.cu = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(C, sb));
+    q.upr = (uint32_t)ceil_div(sb, q.cu);
+    unit += (y1 > y0 ? y1 - y0 : 0) * q.upr;
+}
+
+tg_status plan_span_c(const Problem& P, const Window& w, uint32_t C, SpanGeom* g, int only_pass) {
     std::memset(g, 0, sizeof(*g));
+    const uint64_t n = P.n, rho = P.rho, b0 = w.b0, b1 = w.b1;
     g->one = 1.0f;
-    g->rho = rho;
+    g->rho = P.rho;
     g->C = C;
     g->n = n;
     g->b0 = b0;
-    const uint64_t nb = ceil_div(n, rho);
+    g->r_lo = w.r_lo;
+    g->r_hi = w.r_hi;
+    const tg_strategy s = P.s;
     if (s == TG_BB) {
         g->strat = kSpanBB;
         g->W = b1;
@@ -345,37 +508,44 @@ tg_status plan_span_c(tg_strategy s, uint64_t n, uint32_t rho, uint64_t b0, uint
         g->vb_count = side * side;  // balanced grid (tri.cpp:23-26) incl. padding
         g->units = ceil_div(g->vb_count, C);
     } else if (s == TG_REC) {
-        if (b0 != 0 || b1 != nb) return fail(TG_EINVAL, "rec cannot be sharded");
         g->strat = kSpanREC;
-        uint64_t m;
-        uint32_t k;
-        rec_decompose(n, rho, &m, &k);
-        g->m = m;
-        // unit order: the diagonal pass and the small low levels first (many short
-        // runs per unit, slow warps) so they do not form the launch's tail; the
-        // big square passes, whose units are uniform full runs, come last
-        // (the passes are independent)
-        // A pass whose squares are narrower than C blocks gets units of one block
-        // row (cu = sb): a unit is then one run instead of C / sb short runs
-        // walked by one warp.
+        g->m = P.m;
+        // unit order: the diagonal pass and the small low levels first (many
+        // short runs, slow warps) so they do not form the launch's tail; the big
+        // square passes, whose units are uniform full runs, come last (the
+        // passes are independent).  A pass narrower than C blocks gets units of
+        // one block row (cu = sb).
+        const auto qs = rec_passes(P);
         uint64_t unit = 0;
-        int p = 0;
-        const uint64_t sb0 = m / rho;
-        const uint32_t cu0 = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(C, sb0));
-        g->pass[p] = RecPass{unit, sb0 * sb0 * (1ull << k), sb0, m, 0, cu0};
-        unit += ceil_div(g->pass[p].vb_count, cu0);
-        ++p;
-        for (uint32_t level = 1; level <= k; ++level, ++p) {
-            const uint64_t side = m << (level - 1), sb = side / rho;
-            const uint32_t cu = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(C, sb));
-            g->pass[p] = RecPass{unit, sb * sb * (1ull << (k - level)), sb, side, level, cu};
-            unit += ceil_div(g->pass[p].vb_count, cu);
+        for (size_t t = 0; t < qs.size(); ++t) {
+            const size_t pi = (t == 0) ? qs.size() - 1 : t - 1;  // diag, level 1, ..., level k
+            if (only_pass >= 0 && (size_t)only_pass != pi) continue;
+            const RecPassInfo& q = qs[pi];
+            const uint64_t y0 = rec_row_lower_bound(q, b0), y1 = rec_row_lower_bound(q, b1);
+            add_pass(g, unit, y0, y1, q.sb, q.side, q.level, C);
         }
-        g->npass = p;
         g->units = unit;
-        g->vb_count = 0;
+    } else if (s == TG_RB) {
+        g->strat = kSpanRB;
+        const uint64_t wd = (n % 2 == 0) ? n / 2 : (n + 1) / 2;
+        uint64_t y[4];
+        rb_row_ranges(P, w, y);
+        uint64_t unit = 0;
+        add_pass(g, unit, y[0], y[1], ceil_div(wd, rho), 0, 0, C);  // direct part
+        add_pass(g, unit, y[2], y[3], ceil_div(wd, rho), 0, 1, C);  // folded part
+        g->units = unit;
+    } else if (s == TG_UTM) {
+        g->strat = kSpanUTM;
+        g->engine = P.engine;
+        g->C = utm_blocks_per_unit();
+        g->H = b1 - b0;
+        g->rect_blocks = b0 * g->H;
+        g->u_rect = ceil_div(g->rect_blocks, g->C);
+        g->tri_blocks = tri(g->H);  // = T_nodiag(H + 1) pairs of the block-level UTM
+        g->disc = (2 * g->H + 1) * (2 * g->H + 1);
+        g->units = g->u_rect + ceil_div(g->tri_blocks, g->C);
     } else {
-        return fail(TG_EINVAL, "span mode supports bb, ltm-* and rec");
+        return fail(TG_EINVAL, "span mode: unknown strategy");
     }
     return TG_OK;
 }
@@ -399,45 +569,55 @@ int span_packed() {
 template <int D, int P, bool PK>
 tg_status launch_span_edm_t(const SpanGeom& g, OutWin ow, const float* pts, float* out,
                             const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
-    static int occ = -1;
-    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_edm_kernel<D, P, PK>, kEdmWarps * 32, 0);
-    const uint64_t grid = span_grid(g, persistent, sms, occ, kEdmWarps);
-    if (!grid) return TG_OK;
+    int occ = 1;
+    Scratch qs;  // persistent launches: a per-launch zeroed unit counter (stream-ordered, private)
     unsigned long long* queue = nullptr;
-    if (persistent) {  // dynamic unit queue: a per-launch zeroed counter
-        DeviceCtx* c;
-        TG_TRY(get_ctx(-1, &c));  // the current device (the launch already initialised it)
-        queue = next_queue_for(c);
+    if (persistent) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_edm_kernel<D, P, PK>, kEdmWarps * 32, 0) !=
+            cudaSuccess)
+            occ = 1;
+        TG_TRY(scratch_alloc(qs, sizeof(unsigned long long), st));
+        queue = static_cast<unsigned long long*>(qs.p);
         TG_CUDA(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
     }
+    const uint64_t grid = span_grid(g, persistent, sms, occ, kEdmWarps);
+    if (!grid) return TG_OK;
     span_edm_kernel<D, P, PK><<<(unsigned)grid, kEdmWarps * 32, 0, st>>>(g, ow, pts, out, flag, queue);
     ++g_launches;
     TG_CUDA(cudaGetLastError());
     return TG_OK;
 }
 
-template <int P>
-tg_status launch_span_edm_p(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
-                            const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
-    const bool pk = span_packed() != 0;
-#define TG_EDM_CASE(DD)                                                                          \
-    case DD:                                                                                     \
-        return pk ? launch_span_edm_t<DD, P, true>(g, ow, pts, out, flag, st, persistent, sms)   \
-                  : launch_span_edm_t<DD, P, false>(g, ow, pts, out, flag, st, persistent, sms);
+// The A/B variants (1 chunk slot per lane, scalar instead of f32x2 row pairs)
+// are compiled only into -DTG_AB_VARIANTS=1 builds (build.py --variant): they
+// triple the compile time of the default library for switches that lost.
+#ifndef TG_AB_VARIANTS
+#define TG_AB_VARIANTS 0
+#endif
+
+template <int P, bool PK>
+tg_status launch_span_edm_pk(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
+                             const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
     switch (d) {
-        TG_EDM_CASE(1)
-        TG_EDM_CASE(2)
-        TG_EDM_CASE(3)
-        TG_EDM_CASE(4)
+        case 1: return launch_span_edm_t<1, P, PK>(g, ow, pts, out, flag, st, persistent, sms);
+        case 2: return launch_span_edm_t<2, P, PK>(g, ow, pts, out, flag, st, persistent, sms);
+        case 3: return launch_span_edm_t<3, P, PK>(g, ow, pts, out, flag, st, persistent, sms);
+        case 4: return launch_span_edm_t<4, P, PK>(g, ow, pts, out, flag, st, persistent, sms);
     }
-#undef TG_EDM_CASE
     return fail(TG_EINVAL, "span EDM supports d in [1, 4]");
 }
 
 tg_status launch_span_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
                           const unsigned int* flag, cudaStream_t st, bool persistent, int sms) {
-    return span_slots() == 2 ? launch_span_edm_p<2>(d, g, ow, pts, out, flag, st, persistent, sms)
-                             : launch_span_edm_p<1>(d, g, ow, pts, out, flag, st, persistent, sms);
+    const bool pk = span_packed() != 0, two = span_slots() == 2;
+#if TG_AB_VARIANTS
+    if (!pk) return two ? launch_span_edm_pk<2, false>(d, g, ow, pts, out, flag, st, persistent, sms)
+                        : launch_span_edm_pk<1, false>(d, g, ow, pts, out, flag, st, persistent, sms);
+    if (!two) return launch_span_edm_pk<1, true>(d, g, ow, pts, out, flag, st, persistent, sms);
+#else
+    if (!pk || !two) return fail(TG_EINVAL, "TG_SPAN_PACKED=0 / TG_SPAN_SLOTS=1 need a -DTG_AB_VARIANTS=1 build");
+#endif
+    return launch_span_edm_pk<2, true>(d, g, ow, pts, out, flag, st, persistent, sms);
 }
 
 // A/B switch: TG_WIDE_V1=1 keeps the first d > 4 kernel (per-run transposed staging).
@@ -461,13 +641,8 @@ tg_status launch_wide2_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float
     transpose_points_kernel<<<dim3((unsigned)(n_pad / 32), (unsigned)ceil_div(d_pad, 32)), dim3(32, 8), 0, st>>>(
         pts, n, d, n_pad, d_pad, ptsT);
     const size_t smem = kW2Groups * kW2GroupFloats * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-        TG_CUDA(cudaFuncSetAttribute(wide2_edm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
-    static int occ = -1;
-    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_edm_kernel, kW2Threads, smem);
+    TG_TRY(ensure_smem_attr(c, c->attr_wide2, wide2_edm_kernel, smem));
+    const int occ = occupancy(c->occ_wide2, wide2_edm_kernel, kW2Threads, smem);
     const uint64_t grid =
         std::min<uint64_t>(ceil_div(g.units, kW2Groups), (uint64_t)sms * std::max(occ, 1) * (persistent ? 1 : 64));
     if (!grid) return TG_OK;
@@ -484,8 +659,8 @@ tg_status launch_wide_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float*
     if (!wide_v1()) return launch_wide2_edm(d, g, ow, pts, out, flag, st, persistent, sms, c);
     uint64_t grid = std::min<uint64_t>(g.units, 0x7fffffffull);
     if (persistent) {
-        static int occ = -1;
-        if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide_edm_kernel, 256, 0);
+        int occ = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide_edm_kernel, 256, 0) != cudaSuccess) occ = 1;
         grid = std::min<uint64_t>(grid, (uint64_t)sms * std::max(occ, 1));
     }
     if (!grid) return TG_OK;
@@ -499,12 +674,9 @@ tg_status launch_wide_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float*
 // the rho-block triangle: 128-row tiles covering those rows, tile lambda
 // range [T(ty0), T(ty1)), rows and elements clipped to the window.
 tg_status launch_gram_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, uint64_t b1, OutWin ow,
-                          const float* pts, float* out, float* norms, cudaStream_t st, int sms) {
-    static bool attr = false;
-    if (!attr) {
-        TG_CUDA(cudaFuncSetAttribute(gram_edm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmemBytes));
-        attr = true;
-    }
+                          const float* pts, float* out, float* norms, cudaStream_t st, DeviceCtx* c) {
+    const int sms = c->sms;
+    TG_TRY(ensure_smem_attr(c, c->attr_gram, gram_edm_kernel, kGSmemBytes));
     const uint64_t r0 = std::min<uint64_t>(n, b0 * rho), r1 = std::min<uint64_t>(n, b1 * rho);
     if (r1 <= r0) return TG_OK;
     GramGeom g{};
@@ -543,11 +715,7 @@ bool gram_v1() {
 // max |x|) -> split (hi/lo operands in UMMA layout) -> warp-specialised kernel.
 tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, uint64_t b1, OutWin ow,
                            const float* pts, float* out, DeviceCtx* c, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        TG_CUDA(cudaFuncSetAttribute(gram2_edm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kG2SmemMax));
-        attr = true;
-    }
+    TG_TRY(ensure_smem_attr(c, c->attr_gram2, gram2_edm_kernel, kG2SmemMax));
     const uint64_t r0 = std::min<uint64_t>(n, b0 * rho), r1 = std::min<uint64_t>(n, b1 * rho);
     if (r1 <= r0) return TG_OK;
     const uint32_t nk = (uint32_t)ceil_div(d, 64);
@@ -602,14 +770,17 @@ tg_status launch_classify(const float* pts, uint64_t count, unsigned int* flag, 
     return TG_OK;
 }
 
-template <int P>
+template <int P, int OP>
 tg_status launch_span_write_p(const SpanGeom& g, OutWin ow, uint32_t* out, cudaStream_t st,
                               bool persistent, int sms) {
-    static int occ = -1;
-    if (occ < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_write_kernel<P>, kWarpsPerCta * 32, 0);
+    int occ = 1;
+    if (persistent &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, span_write_kernel<P, OP>, kWarpsPerCta * 32, 0) !=
+            cudaSuccess)
+        occ = 1;
     const uint64_t grid = span_grid(g, persistent, sms, occ);
     if (!grid) return TG_OK;
-    span_write_kernel<P><<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, ow, out);
+    span_write_kernel<P, OP><<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, ow, out);
     ++g_launches;
     TG_CUDA(cudaGetLastError());
     return TG_OK;
@@ -627,13 +798,26 @@ int write_slots() {
 
 tg_status launch_span_write(const SpanGeom& g, OutWin ow, uint32_t* out, cudaStream_t st,
                             bool persistent, int sms) {
-    return write_slots() == 2 ? launch_span_write_p<2>(g, ow, out, st, persistent, sms)
-                              : launch_span_write_p<1>(g, ow, out, st, persistent, sms);
+#if TG_AB_VARIANTS
+    if (write_slots() == 1) return launch_span_write_p<1, kOpWrite>(g, ow, out, st, persistent, sms);
+#else
+    if (write_slots() == 1) return fail(TG_EINVAL, "TG_WRITE_SLOTS=1 needs a -DTG_AB_VARIANTS=1 build");
+#endif
+    return launch_span_write_p<2, kOpWrite>(g, ow, out, st, persistent, sms);
+}
+
+// Span COUNT: +1 per cell of every owned chunk (same walk as the write kernel).
+tg_status launch_span_count(const SpanGeom& g, OutWin ow, uint32_t* out, cudaStream_t st, bool persistent,
+                            int sms) {
+    return launch_span_write_p<2, kOpCount>(g, ow, out, st, persistent, sms);
 }
 
 // --------------------------------------------------------- grid planning
 
-std::vector<GridGeom> plan_grid(tg_strategy s, uint64_t n, uint32_t rho) {
+std::vector<GridGeom> plan_grid(const Problem& P) {
+    const tg_strategy s = P.s;
+    const uint64_t n = P.n;
+    const uint32_t rho = P.rho;
     std::vector<GridGeom> passes;
     GridGeom g{};
     g.rho = rho;
@@ -654,7 +838,7 @@ std::vector<GridGeom> plan_grid(tg_strategy s, uint64_t n, uint32_t rho) {
         passes.push_back(g);
     } else if (s == TG_UTM) {
         g.strat = kGridUTM;
-        g.engine = kNewton;  // parse_strategy("utm") (strategies.cpp:24)
+        g.engine = P.engine;  // newton unless the StrategyId says otherwise (strategies.cpp:24)
         g.pairs = tri_nd(n);
         g.disc_base = (2 * n - 1) * (2 * n - 1);
         const uint64_t tpb = (uint64_t)rho * rho;
@@ -668,9 +852,8 @@ std::vector<GridGeom> plan_grid(tg_strategy s, uint64_t n, uint32_t rho) {
         g.vb_count = g.blocks_x * ceil_div(h, rho);
         passes.push_back(g);
     } else {  // REC: k square passes + 1 diagonal pass, one launch each
-        uint64_t m;
-        uint32_t k;
-        rec_decompose(n, rho, &m, &k);
+        const uint64_t m = P.m;
+        const uint32_t k = P.k;
         g.m = m;
         for (uint32_t level = 1; level <= k; ++level) {
             GridGeom p = g;
@@ -692,9 +875,15 @@ std::vector<GridGeom> plan_grid(tg_strategy s, uint64_t n, uint32_t rho) {
     return passes;
 }
 
+// One launch per grid pass (run_strategy's pass loop, engine.cpp:87-133);
+// marks (optional, passes.size() + 1 events) bracket the passes for per-pass
+// device times.
 template <class Body>
-tg_status launch_grid(const std::vector<GridGeom>& passes, Body body, cudaStream_t st) {
-    for (const GridGeom& g : passes) {
+tg_status launch_grid(const std::vector<GridGeom>& passes, Body body, cudaStream_t st,
+                      const std::vector<cudaEvent_t>* marks = nullptr) {
+    for (size_t p = 0; p < passes.size(); ++p) {
+        const GridGeom& g = passes[p];
+        if (marks) TG_CUDA(cudaEventRecord((*marks)[p], st));
         if (g.vb_count == 0) continue;
         const uint32_t threads = std::min<uint32_t>(g.rho * g.rho, 1024);
         const uint64_t blocks = std::min<uint64_t>(g.vb_count, 0x7fffffffull);
@@ -702,6 +891,7 @@ tg_status launch_grid(const std::vector<GridGeom>& passes, Body body, cudaStream
         ++g_launches;
         TG_CUDA(cudaGetLastError());
     }
+    if (marks) TG_CUDA(cudaEventRecord(marks->back(), st));
     return TG_OK;
 }
 
@@ -754,6 +944,183 @@ bool resolve_span(const tg_launch_opts& o, tg_strategy s, uint32_t rho, bool bod
     return o.mode == TG_MODE_SPAN ? true : ok;
 }
 
+// A/B switch: TG_COLLIDE_V1=1 keeps the first span collision kernel (one pair per lane per word).
+bool collide_v1() {
+    static bool v = [] {
+        const char* e = std::getenv("TG_COLLIDE_V1");
+        return e && std::atoi(e) != 0;
+    }();
+    return v;
+}
+
+// The td-kernel launch behind tg_launch (launch_dummy / launch_edm /
+// launch_count / launch, engine.cpp:150-203) for a validated problem.  Per-pass
+// device times go to o.per_pass (LaunchOptions::per_pass, engine.cpp:87-133):
+// REC's passes are then launched one by one, bracketed by events.
+tg_status launch_impl(tg_kernel kernel, const Problem& P, uint32_t d, const float* pts, void* out,
+                      const tg_launch_opts& o, tg_dispatch_stats* stats) {
+    const tg_strategy s = P.s;
+    const uint64_t n = P.n;
+    const uint32_t rho = P.rho;
+    const uint32_t G = o.shard_count == 0 ? 1 : o.shard_count;
+    tg_dispatch_stats st_local;
+    std::vector<tg_dispatch_stats> pp;
+    TG_TRY(stats_for(P, o.shard_index, G, &st_local, &pp));
+    if (o.per_pass && o.per_pass_cap < pp.size())
+        return fail(TG_EINVAL, "per_pass: buffer holds fewer entries than the strategy's grid passes");
+    auto report = [&](bool timed_passes) {
+        if (stats) *stats = st_local;
+        if (o.per_pass) {
+            for (size_t p = 0; p < pp.size(); ++p) {
+                if (!timed_passes) pp[p].wall_time_ns = pp.size() == 1 ? st_local.wall_time_ns : 0;
+                o.per_pass[p] = pp[p];
+            }
+        }
+        return TG_OK;
+    };
+    if (G > 1 && kernel != TG_KERNEL_DUMMY) {
+        uint64_t eb, ee;
+        TG_TRY(tg_shard_elems(n, rho, o.shard_index, G, 1, &eb, &ee));
+        if (ee == eb) return report(false);  // empty shard (more shards than block rows): nothing to do
+    }
+    if (kernel == TG_KERNEL_EDM) {
+        if (d < 1) return fail(TG_EINVAL, "launch_edm: features must be >= 1");
+        if (!pts || !out) return fail(TG_EINVAL, "launch: EDM kernel needs points and an output buffer");
+        if (reinterpret_cast<uintptr_t>(pts) % 16 != 0)
+            return fail(TG_EINVAL, "launch_edm: device points must be 16-byte aligned");
+    }
+    if ((kernel == TG_KERNEL_WRITE || kernel == TG_KERNEL_COUNT) && !out)
+        return fail(TG_EINVAL, "launch: output buffer is NULL");
+    if (kernel == TG_KERNEL_EDM || kernel == TG_KERNEL_WRITE) {
+        if (reinterpret_cast<uintptr_t>(out) % 16 != 0)
+            return fail(TG_EINVAL, "launch: device output must be 16-byte aligned");
+    }
+    if ((int)kernel < 0 || (int)kernel > (int)TG_KERNEL_COUNT) return fail(TG_EINVAL, "launch: unknown kernel kind");
+    DeviceCtx* c;
+    TG_TRY(get_ctx(o.device, &c));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(o.stream);
+    const Window w = window_of(P, o.shard_index, G);
+    const OutWin ow{tri(w.r_lo), tri(w.r_hi)};
+    if (o.mode == TG_MODE_GRAM) {
+        if (kernel != TG_KERNEL_EDM) return fail(TG_EINVAL, "gram mode computes the EDM only");
+        if (!(is_ltm(s) || s == TG_BB))
+            return fail(TG_EINVAL, "gram mode tiles the triangle by g(lambda) (bb / ltm-* strategies)");
+        Timer timer(st, !o.async);
+        if (!gram_v1()) {
+            TG_TRY(launch_gram2_edm(n, d, rho, w.b0, w.b1, ow, pts, static_cast<float*>(out), c, st));
+        } else {
+            Scratch sn;
+            TG_TRY(scratch_alloc(sn, n * sizeof(float), st));
+            TG_TRY(launch_gram_edm(n, d, rho, w.b0, w.b1, ow, pts, static_cast<float*>(out),
+                                   static_cast<float*>(sn.p), st, c));
+        }
+        TG_TRY(timer.finish(&st_local));
+        return report(false);
+    }
+    // the dummy kernel runs in span form only on request: AUTO keeps the
+    // paper's one-thread-per-cell dummy so the mapping comparison (I vs BB)
+    // of the reference protocol stays within one execution shape
+    const bool body_span = (kernel == TG_KERNEL_EDM && (d <= 4 || (rho == 16 && square_tiles(s)))) ||
+                           kernel == TG_KERNEL_WRITE || kernel == TG_KERNEL_COUNT ||
+                           (kernel == TG_KERNEL_DUMMY && o.mode == TG_MODE_SPAN);
+    const bool span = resolve_span(o, s, rho, body_span);
+    if (span && !(body_span && span_eligible(s, rho)))
+        return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec/rb (rho % 4 == 0) or utm (rho a power of two in "
+                               "[4, 128]) and an edm (d <= 4; d > 4 with rho == 16 for bb/ltm-*/rec), write, "
+                               "count or dummy body");
+    if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode");
+
+    const bool timed_passes = o.per_pass && !o.async && pp.size() > 1;
+    std::vector<cudaEvent_t> marks;
+    struct EvGuard {
+        std::vector<cudaEvent_t>& v;
+        ~EvGuard() {
+            for (auto e : v) cudaEventDestroy(e);
+        }
+    } evg{marks};
+    if (timed_passes) {
+        marks.resize(pp.size() + 1);
+        for (auto& e : marks) TG_CUDA(cudaEventCreate(&e));
+    }
+    Timer timer(st, !o.async);
+    if (span) {
+        const bool wide = kernel == TG_KERNEL_EDM && d > 4;
+        const int slots = wide ? 1 : ((kernel == TG_KERNEL_WRITE || kernel == TG_KERNEL_COUNT) ? write_slots()
+                                                                                              : span_slots());
+        const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * slots) / rho);
+        Scratch fs;
+        unsigned int* flag = nullptr;
+        if (kernel == TG_KERNEL_EDM) {  // per-launch classify verdict (stream-ordered, private)
+            TG_TRY(scratch_alloc(fs, sizeof(unsigned int), st));
+            flag = static_cast<unsigned int*>(fs.p);
+            TG_TRY(launch_classify(pts, n * d, flag, st, c->sms));
+        }
+        // REC with per-pass timing: one launch per grid pass, reference order
+        const int npl = (timed_passes && s == TG_REC) ? (int)pp.size() : 1;
+        for (int pl = 0; pl < npl; ++pl) {
+            SpanGeom g;
+            TG_TRY(plan_span(P, w, C, &g, !wide, npl > 1 ? pl : -1));
+            if (timed_passes) TG_CUDA(cudaEventRecord(marks[pl], st));
+            if (kernel == TG_KERNEL_EDM) {
+                if (d <= 4) {
+                    TG_TRY(launch_span_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0,
+                                           c->sms));
+                } else {
+                    TG_TRY(launch_wide_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0,
+                                           c->sms, c));
+                }
+            } else if (kernel == TG_KERNEL_DUMMY) {
+                auto* sink = o.sink ? static_cast<unsigned long long*>(o.sink) : c->scratch;
+                const uint64_t grid = span_grid(g, o.persistent != 0, c->sms, 8);
+                if (grid) {
+                    span_dummy_kernel<<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, sink, o.sentinel);
+                    ++g_launches;
+                    TG_CUDA(cudaGetLastError());
+                }
+            } else if (kernel == TG_KERNEL_COUNT) {
+                TG_TRY(launch_span_count(g, ow, static_cast<uint32_t*>(out), st, o.persistent != 0, c->sms));
+            } else {
+                TG_TRY(launch_span_write(g, ow, static_cast<uint32_t*>(out), st, o.persistent != 0, c->sms));
+            }
+        }
+        if (timed_passes) {
+            if (npl == 1)  // single span launch for a multi-pass grid: time it as a whole
+                for (size_t p = 1; p < marks.size() - 1; ++p) TG_CUDA(cudaEventRecord(marks[p], st));
+            TG_CUDA(cudaEventRecord(marks.back(), st));
+        }
+    } else {
+        const auto passes = plan_grid(P);
+        const std::vector<cudaEvent_t>* mk = timed_passes ? &marks : nullptr;
+        switch (kernel) {
+            case TG_KERNEL_EDM:
+                TG_TRY(launch_grid(passes, EdmBody{pts, static_cast<float*>(out), d}, st, mk));
+                if (s == TG_UTM) TG_TRY(launch_diag_fill(static_cast<float*>(out), n, false, st, c->sms));
+                break;
+            case TG_KERNEL_WRITE:
+                TG_TRY(launch_grid(passes, WriteBody{static_cast<uint32_t*>(out)}, st, mk));
+                if (s == TG_UTM) TG_TRY(launch_diag_fill(static_cast<uint32_t*>(out), n, true, st, c->sms));
+                break;
+            case TG_KERNEL_COUNT:
+                TG_TRY(launch_grid(passes, CountBody{static_cast<uint32_t*>(out)}, st, mk));
+                break;
+            default: {  // TG_KERNEL_DUMMY
+                auto* sink = o.sink ? static_cast<unsigned long long*>(o.sink) : c->scratch;
+                TG_TRY(launch_grid(passes, DummyBody{sink, o.sentinel}, st, mk));
+                break;
+            }
+        }
+    }
+    TG_TRY(timer.finish(&st_local));
+    if (timed_passes) {
+        for (size_t p = 0; p < pp.size(); ++p) {
+            float ms = 0;
+            TG_CUDA(cudaEventElapsedTime(&ms, marks[p], marks[p + 1]));
+            pp[p].wall_time_ns = (uint64_t)std::llround((double)ms * 1e6);
+        }
+    }
+    return report(timed_passes);
+}
+
 }  // namespace
 
 // ======================================================================
@@ -764,6 +1131,7 @@ void tg_launch_opts_init(tg_launch_opts* o) {
     o->device = -1;
     o->mode = TG_MODE_AUTO;
     o->sentinel = ~0ull;
+    o->engine = -1;
 }
 
 const char* tg_last_error(void) { return g_err.c_str(); }
@@ -920,129 +1288,10 @@ tg_status tg_launch(tg_kernel kernel, tg_strategy s, uint64_t n, uint32_t d, uin
                     tg_dispatch_stats* stats) {
     g_launches = 0;
     const tg_launch_opts o = opts ? *opts : default_opts();
-    TG_TRY(validate_problem(s, n, rho));
-    const uint32_t G = o.shard_count == 0 ? 1 : o.shard_count;
-    tg_dispatch_stats st_local;
-    TG_TRY(stats_for(s, n, rho, o.shard_index, G, &st_local));
-    if (G > 1 && (kernel == TG_KERNEL_EDM || kernel == TG_KERNEL_WRITE)) {
-        uint64_t eb, ee;
-        TG_TRY(tg_shard_elems(n, rho, o.shard_index, G, 1, &eb, &ee));
-        if (ee == eb) {  // empty shard (more shards than block rows): nothing to do
-            if (stats) *stats = st_local;
-            return TG_OK;
-        }
-    }
-    if (kernel == TG_KERNEL_EDM) {
-        if (d < 1) return fail(TG_EINVAL, "launch_edm: features must be >= 1");
-        if (!pts || !out) return fail(TG_EINVAL, "launch: EDM kernel needs points and an output buffer");
-        if (reinterpret_cast<uintptr_t>(pts) % 16 != 0)
-            return fail(TG_EINVAL, "launch_edm: device points must be 16-byte aligned");
-    }
-    if ((kernel == TG_KERNEL_WRITE || kernel == TG_KERNEL_COUNT) && !out)
-        return fail(TG_EINVAL, "launch: output buffer is NULL");
-    if (kernel == TG_KERNEL_EDM || kernel == TG_KERNEL_WRITE) {
-        if (reinterpret_cast<uintptr_t>(out) % 16 != 0)
-            return fail(TG_EINVAL, "launch: device output must be 16-byte aligned");
-    }
-    DeviceCtx* c;
-    TG_TRY(get_ctx(o.device, &c));
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(o.stream);
-    if (o.mode == TG_MODE_GRAM) {
-        if (kernel != TG_KERNEL_EDM) return fail(TG_EINVAL, "gram mode computes the EDM only");
-        if (!(is_ltm(s) || s == TG_BB))
-            return fail(TG_EINVAL, "gram mode tiles the triangle by g(lambda) (bb / ltm-* strategies)");
-        const uint64_t nb = ceil_div(n, rho);
-        const auto rows = shard_rows(nb, G);
-        const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
-        OutWin ow{tri(std::min<uint64_t>(n, b0 * rho)), tri(std::min<uint64_t>(n, b1 * rho))};
-        Timer timer(st, !o.async);
-        if (!gram_v1()) {
-            TG_TRY(launch_gram2_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out), c, st));
-        } else {
-            Scratch sn;
-            TG_TRY(scratch_alloc(sn, n * sizeof(float), st));
-            TG_TRY(launch_gram_edm(n, d, rho, b0, b1, ow, pts, static_cast<float*>(out), static_cast<float*>(sn.p),
-                                   st, c->sms));
-        }
-        TG_TRY(timer.finish(&st_local));
-        if (stats) *stats = st_local;
-        return TG_OK;
-    }
-    // the dummy kernel runs in span form only on request: AUTO keeps the
-    // paper's one-thread-per-cell dummy so the mapping comparison (I vs BB)
-    // of the reference protocol stays within one execution shape
-    const bool body_span = (kernel == TG_KERNEL_EDM && (d <= 4 || rho == 16)) || kernel == TG_KERNEL_WRITE ||
-                           (kernel == TG_KERNEL_DUMMY && o.mode == TG_MODE_SPAN);
-    const bool span = resolve_span(o, s, rho, body_span);
-    if (span && !(body_span && span_eligible(s, rho)))
-        return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec, rho % 4 == 0 and an edm (d<=4), write or dummy body");
-    if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode (bb/ltm-*)");
-
-    Timer timer(st, !o.async);
-    if (span) {
-        const uint64_t nb = ceil_div(n, rho);
-        const auto rows = shard_rows(nb, G);
-        const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
-        SpanGeom g;
-        const bool wide = kernel == TG_KERNEL_EDM && d > 4;
-        const int slots = wide ? 1 : (kernel == TG_KERNEL_WRITE ? write_slots() : span_slots());
-        const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * slots) / rho);
-        TG_TRY(plan_span(s, n, rho, b0, b1, C, &g, !wide));
-        OutWin ow{tri(std::min<uint64_t>(n, b0 * rho)), tri(std::min<uint64_t>(n, b1 * rho))};
-        if (kernel == TG_KERNEL_EDM) {
-            unsigned int* flag = next_flag(c);
-            TG_TRY(launch_classify(pts, n * d, flag, st, c->sms));
-            if (d <= 4) {
-                TG_TRY(launch_span_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms));
-            } else {
-                TG_TRY(launch_wide_edm(d, g, ow, pts, static_cast<float*>(out), flag, st, o.persistent != 0, c->sms, c));
-            }
-        } else if (kernel == TG_KERNEL_DUMMY) {
-            auto* sink = o.sink ? static_cast<unsigned long long*>(o.sink) : c->scratch;
-            const uint64_t grid = span_grid(g, o.persistent != 0, c->sms, 8);
-            if (grid) {
-                span_dummy_kernel<<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(g, sink, o.sentinel);
-                ++g_launches;
-                TG_CUDA(cudaGetLastError());
-            }
-        } else {
-            TG_TRY(launch_span_write(g, ow, static_cast<uint32_t*>(out), st, o.persistent != 0, c->sms));
-        }
-    } else {
-        const auto passes = plan_grid(s, n, rho);
-        switch (kernel) {
-            case TG_KERNEL_EDM:
-                TG_TRY(launch_grid(passes, EdmBody{pts, static_cast<float*>(out), d}, st));
-                if (s == TG_UTM) TG_TRY(launch_diag_fill(static_cast<float*>(out), n, false, st, c->sms));
-                break;
-            case TG_KERNEL_WRITE:
-                TG_TRY(launch_grid(passes, WriteBody{static_cast<uint32_t*>(out)}, st));
-                if (s == TG_UTM) TG_TRY(launch_diag_fill(static_cast<uint32_t*>(out), n, true, st, c->sms));
-                break;
-            case TG_KERNEL_COUNT:
-                TG_TRY(launch_grid(passes, CountBody{static_cast<uint32_t*>(out)}, st));
-                break;
-            case TG_KERNEL_DUMMY: {
-                auto* sink = o.sink ? static_cast<unsigned long long*>(o.sink) : c->scratch;
-                TG_TRY(launch_grid(passes, DummyBody{sink, o.sentinel}, st));
-                break;
-            }
-            default:
-                return fail(TG_EINVAL, "launch: unknown kernel kind");
-        }
-    }
-    TG_TRY(timer.finish(&st_local));
-    if (stats) *stats = st_local;
-    return TG_OK;
-}
-
-// A/B switch: TG_COLLIDE_V1=1 keeps the first span collision kernel (one pair per lane per word).
-bool collide_v1() {
-    static bool v = [] {
-        const char* e = std::getenv("TG_COLLIDE_V1");
-        return e && std::atoi(e) != 0;
-    }();
-    return v;
+    Problem P;
+    TG_TRY(make_problem(s, n, rho, &o, &P));
+    DevGuard guard;
+    return launch_impl(kernel, P, d, pts, out, o, stats);
 }
 
 tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spheres, float r_max,
@@ -1050,30 +1299,30 @@ tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spher
                      tg_dispatch_stats* stats) {
     g_launches = 0;
     const tg_launch_opts o = opts ? *opts : default_opts();
-    TG_TRY(validate_problem(s, n, rho));
+    Problem P;
+    TG_TRY(make_problem(s, n, rho, &o, &P));
     if (!spheres || !bits || !hits) return fail(TG_EINVAL, "collide: NULL buffer");
     if (reinterpret_cast<uintptr_t>(spheres) % 16 != 0)
         return fail(TG_EINVAL, "collide: spheres must be 16-byte aligned");
     const uint32_t G = o.shard_count == 0 ? 1 : o.shard_count;
     tg_dispatch_stats st_local;
-    TG_TRY(stats_for(s, n, rho, o.shard_index, G, &st_local));
+    TG_TRY(stats_for(P, o.shard_index, G, &st_local));
+    DevGuard guard;
     DeviceCtx* c;
     TG_TRY(get_ctx(o.device, &c));
     cudaStream_t st = reinterpret_cast<cudaStream_t>(o.stream);
-    const bool span = resolve_span(o, s, rho, true);
-    if (span && !span_eligible(s, rho)) return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec and rho % 4 == 0");
-    if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode (bb/ltm-*)");
+    const bool ok_span = span_eligible(s, rho) && (square_tiles(s) || s == TG_RB);
+    const bool span = resolve_span(o, s, rho, ok_span);
+    if (span && !ok_span) return fail(TG_EINVAL, "span collide needs bb/ltm-*/rec/rb and rho % 4 == 0");
+    if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode");
     uint64_t p0, p1;
     TG_TRY(tg_shard_elems(n, rho, o.shard_index, G, 0, &p0, &p1));
     Timer timer(st, !o.async);
     TG_CUDA(cudaMemsetAsync(hits, 0, sizeof(uint64_t), st));
     if (span) {
-        const uint64_t nb = ceil_div(n, rho);
-        const auto rows = shard_rows(nb, G);
+        const Window w = window_of(P, o.shard_index, G);
         SpanGeom g;
-        // v2: runs of up to 256 columns (8 column slots per lane)
-        TG_TRY(plan_span(s, n, rho, rows[o.shard_index], rows[o.shard_index + 1],
-                         std::max<uint32_t>(1, (collide_v1() ? 128 : 32 * TG_COLLIDE_SLOTS) / rho), &g));
+        TG_TRY(plan_span(P, w, std::max<uint32_t>(1, (collide_v1() ? 128 : 32 * TG_COLLIDE_SLOTS) / rho), &g));
         const uint64_t grid = span_grid(g, o.persistent != 0, c->sms, 8);
         if (grid && collide_v1()) {
             span_collide_kernel<<<(unsigned)grid, kWarpsPerCta * 32, 0, st>>>(
@@ -1093,7 +1342,7 @@ tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spher
         }
     } else {
         TG_CUDA(cudaMemsetAsync(bits, 0, ceil_div(p1 - p0, 32) * 4, st));
-        TG_TRY(launch_grid(plan_grid(s, n, rho),
+        TG_TRY(launch_grid(plan_grid(P),
                            CollideBody{reinterpret_cast<const float4*>(spheres), r_max, bits,
                                        reinterpret_cast<unsigned long long*>(hits)},
                            st));
@@ -1103,30 +1352,31 @@ tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spher
     return TG_OK;
 }
 
-tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint32_t d,
-                               uint32_t rho, float* out, const tg_launch_opts* opts,
-                               tg_dispatch_stats* stats) {
-    g_launches = 0;
-    const tg_launch_opts o = opts ? *opts : default_opts();
-    TG_TRY(validate_problem(s, n, rho));
-    if (d < 1 || d > 4) return fail(TG_EINVAL, "launch_edm: features must be in [1, 4]");
-    if (!pts || !out) return fail(TG_EINVAL, "launch: EDM kernel needs points and an output buffer");
-    const uint32_t G = o.shard_count == 0 ? 1 : o.shard_count;
-    tg_dispatch_stats st_local;
-    TG_TRY(stats_for(s, n, rho, o.shard_index, G, &st_local));
-    DeviceCtx* c;
-    TG_TRY(get_ctx(o.device, &c));
-    std::lock_guard<std::mutex> lk(c->mu);
-    cudaStream_t st = o.stream ? reinterpret_cast<cudaStream_t>(o.stream) : c->stream;
-    const bool span = resolve_span(o, s, rho, true);
-    if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode (bb/ltm-*)");
-    if (span && !span_eligible(s, rho)) return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec and rho % 4 == 0");
+}  // extern "C"
 
-    const uint64_t nb = ceil_div(n, rho);
-    const auto rows = shard_rows(nb, G);
-    const uint64_t b0 = rows[o.shard_index], b1 = rows[o.shard_index + 1];
-    const uint64_t eb = tri(std::min<uint64_t>(n, b0 * rho)), ee = tri(std::min<uint64_t>(n, b1 * rho));
+namespace {
+
+// One device's part of tg_edm_strategy_host: lambda-range shard `shard` of G
+// of problem P, host points in, the shard's packed slice out (host).  The
+// kernel runs in block-row pieces whose D2H copies overlap the next piece.
+tg_status edm_host_shard(const Problem& P, const float* pts, uint32_t d, float* out, const tg_launch_opts& o,
+                         int device, uint32_t shard, uint32_t G, uint64_t* wall_ns) {
+    const uint64_t n = P.n;
+    const uint32_t rho = P.rho;
+    DeviceCtx* c;
+    TG_TRY(get_ctx(device, &c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = (o.stream && o.n_devices <= 1) ? reinterpret_cast<cudaStream_t>(o.stream) : c->stream;
+    const bool span = resolve_span(o, P.s, rho, true);
+    if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode");
+    if (span && !span_eligible(P.s, rho))
+        return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec/rb (rho % 4 == 0) or utm (rho a power of two)");
+    const Window w = window_of(P, shard, G);
+    const uint64_t b0 = w.b0, b1 = w.b1;
+    const uint64_t eb = tri(w.r_lo), ee = tri(w.r_hi);
     const uint64_t elems = ee - eb;
+    *wall_ns = 0;
+    if (elems == 0) return TG_OK;
     TG_TRY(ensure_buf(c->bufs[0], n * d * sizeof(float)));
     TG_TRY(ensure_buf(c->bufs[1], elems * sizeof(float)));
     float* d_pts = static_cast<float*>(c->bufs[0].p);
@@ -1135,14 +1385,17 @@ tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint
     TG_CUDA(cudaEventRecord(c->ev[32], st));
     TG_CUDA(cudaMemcpyAsync(d_pts, pts, n * d * sizeof(float), cudaMemcpyHostToDevice, st));
     if (span) {
-        unsigned int* flag = next_flag(c);
+        Scratch fs;
+        TG_TRY(scratch_alloc(fs, sizeof(unsigned int), st));
+        unsigned int* flag = static_cast<unsigned int*>(fs.p);
         TG_TRY(launch_classify(d_pts, n * d, flag, st, c->sms));
-        // Copy pipeline: pieces of block rows, each piece's D2H overlaps the next kernel.
+        // Copy pipeline: pieces of block rows (row windows: every strategy's
+        // piece q writes exactly the packed rows of its window), each piece's
+        // D2H overlapping the next piece's kernel.
         const uint64_t bytes = elems * sizeof(float);
-        uint32_t Q = (s == TG_REC) ? 1 : (uint32_t)std::min<uint64_t>(16, std::max<uint64_t>(1, bytes >> 28));
+        uint32_t Q = (uint32_t)std::min<uint64_t>(16, std::max<uint64_t>(1, bytes >> 28));
         Q = (uint32_t)std::min<uint64_t>(Q, std::max<uint64_t>(1, b1 - b0));
-        // piece bounds: split [b0, b1) by element count
-        std::vector<uint64_t> pr(Q + 1);
+        std::vector<uint64_t> pr(Q + 1);  // piece bounds: [b0, b1) split by element count
         pr[0] = b0;
         pr[Q] = b1;
         for (uint32_t q = 1; q < Q; ++q) {
@@ -1151,14 +1404,15 @@ tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint
             pr[q] = std::min(std::max(r, pr[q - 1]), b1);
         }
         const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * span_slots()) / rho);
-        OutWin ow{eb, ee};
+        const OutWin ow{eb, ee};
         uint64_t lo = 0, sub_k = 0;
         for (uint32_t q = 0; q < Q; ++q) {
+            const Window wq{pr[q], pr[q + 1], std::min<uint64_t>(n, pr[q] * rho), std::min<uint64_t>(n, pr[q + 1] * rho)};
             SpanGeom g;
-            TG_TRY(plan_span(s, n, rho, pr[q], pr[q + 1], C, &g));
+            TG_TRY(plan_span(P, wq, C, &g));
             TG_TRY(launch_span_edm(d, g, ow, d_pts, d_out, flag, st, o.persistent != 0, c->sms));
             TG_CUDA(cudaEventRecord(c->ev[q], st));
-            const uint64_t piece_end = tri(std::min<uint64_t>(n, pr[q + 1] * rho)) - eb;
+            const uint64_t piece_end = tri(wq.r_hi) - eb;
             const uint64_t hi = (q + 1 == Q) ? elems : std::min<uint64_t>(elems, (piece_end + 3) & ~3ull);
             if (hi > lo) {
                 // 256 MB sub-copies alternating two streams: 56 vs 52 GB/s for one
@@ -1176,8 +1430,8 @@ tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint
         }
         TG_CUDA(cudaEventRecord(c->ev[33], st));
     } else {
-        TG_TRY(launch_grid(plan_grid(s, n, rho), EdmBody{d_pts, d_out, d}, st));
-        if (s == TG_UTM) TG_TRY(launch_diag_fill(d_out, n, false, st, c->sms));
+        TG_TRY(launch_grid(plan_grid(P), EdmBody{d_pts, d_out, d}, st));
+        if (P.s == TG_UTM) TG_TRY(launch_diag_fill(d_out, n, false, st, c->sms));
         TG_CUDA(cudaEventRecord(c->ev[33], st));
         TG_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev[33], 0));
         TG_CUDA(cudaMemcpyAsync(out, d_out, elems * sizeof(float), cudaMemcpyDeviceToHost, c->copy_stream));
@@ -1187,33 +1441,236 @@ tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint
     TG_CUDA(cudaStreamSynchronize(st));
     float ms = 0;
     TG_CUDA(cudaEventElapsedTime(&ms, c->ev[32], c->ev[33]));
-    st_local.wall_time_ns = (uint64_t)std::llround((double)ms * 1e6);
-    if (stats) *stats = st_local;
+    *wall_ns = (uint64_t)std::llround((double)ms * 1e6);
     return TG_OK;
 }
 
-tg_status tg_coverage_ok(tg_strategy s, uint64_t n, uint32_t rho, int device, int* ok) {
-    g_launches = 0;
-    TG_TRY(validate_problem(s, n, rho));
-    DeviceCtx* c;
-    TG_TRY(get_ctx(device, &c));
-    std::lock_guard<std::mutex> lk(c->mu);
-    cudaStream_t st = c->stream;
-    const uint64_t cells = tri(n);
-    TG_TRY(ensure_buf(c->bufs[2], cells * sizeof(uint32_t)));
-    uint32_t* counts = static_cast<uint32_t*>(c->bufs[2].p);
-    TG_CUDA(cudaMemsetAsync(counts, 0, cells * sizeof(uint32_t), st));
-    TG_TRY(launch_grid(plan_grid(s, n, rho), CountBody{counts}, st));
+// Coverage verdict of one count table on device: cells of the window that
+// are not touched exactly once (0 on the diagonal for a no-diagonal domain).
+tg_status check_counts(DeviceCtx* c, cudaStream_t st, const uint32_t* counts, uint64_t n, bool with_diag,
+                       uint64_t* bad, uint64_t* first) {
     unsigned long long init[2] = {0, ~0ull};
     TG_CUDA(cudaMemcpyAsync(c->scratch + 1, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    const uint64_t blocks = std::min<uint64_t>(ceil_div(cells, 256), (uint64_t)c->sms * 16);
-    check_counts_kernel<<<(unsigned)blocks, 256, 0, st>>>(counts, n, s != TG_UTM, c->scratch + 1, c->scratch + 2);
+    const uint64_t blocks = std::min<uint64_t>(ceil_div(tri(n), 256), (uint64_t)c->sms * 16);
+    check_counts_kernel<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, st>>>(counts, n, with_diag ? 1 : 0,
+                                                                                  c->scratch + 1, c->scratch + 2);
     ++g_launches;
     TG_CUDA(cudaGetLastError());
     unsigned long long res[2];
     TG_CUDA(cudaMemcpyAsync(res, c->scratch + 1, sizeof(res), cudaMemcpyDeviceToHost, st));
     TG_CUDA(cudaStreamSynchronize(st));
-    *ok = res[0] == 0 ? 1 : 0;
+    *bad = res[0];
+    *first = res[1];
+    return TG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tg_status tg_edm_strategy_host(tg_strategy s, const float* pts, uint64_t n, uint32_t d,
+                               uint32_t rho, float* out, const tg_launch_opts* opts,
+                               tg_dispatch_stats* stats) {
+    g_launches = 0;
+    const tg_launch_opts o = opts ? *opts : default_opts();
+    Problem P;
+    TG_TRY(make_problem(s, n, rho, &o, &P));
+    if (d < 1 || d > 4) return fail(TG_EINVAL, "launch_edm: features must be in [1, 4]");
+    if (!pts || !out) return fail(TG_EINVAL, "launch: EDM kernel needs points and an output buffer");
+    const uint32_t G = o.shard_count == 0 ? 1 : o.shard_count;
+    tg_dispatch_stats st_local;
+    TG_TRY(stats_for(P, o.shard_index, G, &st_local));
+    DevGuard guard;
+    if (o.n_devices <= 1) {
+        const int dev = (o.n_devices == 1 && o.devices) ? o.devices[0] : o.device;
+        TG_TRY(edm_host_shard(P, pts, d, out, o, dev, o.shard_index, G, &st_local.wall_time_ns));
+        if (stats) *stats = st_local;
+        return TG_OK;
+    }
+    // several devices: shard g of n_devices on devices[g], each copying its
+    // slice out over its own link, in parallel host threads
+    if (G > 1) return fail(TG_EINVAL, "edm_strategy: n_devices > 1 splits the whole domain (shard_count must be 0/1)");
+    if (!o.devices) return fail(TG_EINVAL, "edm_strategy: n_devices > 1 needs a devices array");
+    const uint32_t D = o.n_devices;
+    TG_TRY(stats_for(P, 0, 1, &st_local));
+    std::vector<tg_status> rc(D, TG_OK);
+    std::vector<std::string> err(D);
+    std::vector<uint64_t> wall(D, 0);
+    std::vector<std::thread> th;
+    for (uint32_t g = 0; g < D; ++g) {
+        th.emplace_back([&, g] {
+            const Window w = window_of(P, g, D);
+            rc[g] = edm_host_shard(P, pts, d, out + tri(w.r_lo), o, o.devices[g], g, D, &wall[g]);
+            if (rc[g] != TG_OK) err[g] = g_err;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (uint32_t g = 0; g < D; ++g)
+        if (rc[g] != TG_OK) return fail(rc[g], "device " + std::to_string(o.devices[g]) + ": " + err[g]);
+    st_local.wall_time_ns = *std::max_element(wall.begin(), wall.end());
+    if (stats) *stats = st_local;
+    return TG_OK;
+}
+
+tg_status tg_coverage_ok_opts(tg_strategy s, uint64_t n, uint32_t rho, const tg_launch_opts* opts, int* ok,
+                              uint64_t* bad, uint64_t* first_bad) {
+    g_launches = 0;
+    tg_launch_opts o = opts ? *opts : default_opts();
+    Problem P;
+    TG_TRY(make_problem(s, n, rho, &o, &P));
+    o.shard_index = 0;
+    o.shard_count = 1;
+    o.async = 0;
+    o.per_pass = nullptr;
+    DevGuard guard;
+    DeviceCtx* c;
+    TG_TRY(get_ctx(o.device, &c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    o.device = c->dev;
+    o.stream = c->stream;
+    const uint64_t cells = tri(n);
+    TG_TRY(ensure_buf(c->bufs[2], cells * sizeof(uint32_t)));
+    uint32_t* counts = static_cast<uint32_t*>(c->bufs[2].p);
+    TG_CUDA(cudaMemsetAsync(counts, 0, cells * sizeof(uint32_t), c->stream));
+    const uint64_t launches0 = g_launches;
+    TG_TRY(launch_impl(TG_KERNEL_COUNT, P, 0, nullptr, counts, o, nullptr));
+    uint64_t nbad, first;
+    TG_TRY(check_counts(c, c->stream, counts, n, s != TG_UTM, &nbad, &first));
+    g_launches += launches0;
+    *ok = nbad == 0 ? 1 : 0;
+    if (bad) *bad = nbad;
+    if (first_bad) *first_bad = first;
+    return TG_OK;
+}
+
+tg_status tg_coverage_ok(tg_strategy s, uint64_t n, uint32_t rho, int device, int* ok) {
+    tg_launch_opts o = default_opts();
+    o.device = device;
+    return tg_coverage_ok_opts(s, n, rho, &o, ok, nullptr, nullptr);
+}
+
+tg_status tg_count_host(tg_strategy s, uint64_t n, uint32_t rho, uint32_t* counts, const tg_launch_opts* opts,
+                        tg_dispatch_stats* stats) {
+    g_launches = 0;
+    tg_launch_opts o = opts ? *opts : default_opts();
+    Problem P;
+    TG_TRY(make_problem(s, n, rho, &o, &P));
+    if (!counts) return fail(TG_EINVAL, "launch_count: NULL counter buffer");
+    if (o.shard_count > 1) return fail(TG_EINVAL, "launch_count: the host counter vector covers the whole domain");
+    DevGuard guard;
+    DeviceCtx* c;
+    TG_TRY(get_ctx(o.device, &c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    o.device = c->dev;
+    o.stream = c->stream;
+    o.async = 0;
+    const uint64_t bytes = tri(n) * sizeof(uint32_t);
+    TG_TRY(ensure_buf(c->bufs[2], bytes));
+    uint32_t* d = static_cast<uint32_t*>(c->bufs[2].p);
+    TG_CUDA(cudaMemcpyAsync(d, counts, bytes, cudaMemcpyHostToDevice, c->stream));
+    TG_TRY(launch_impl(TG_KERNEL_COUNT, P, 0, nullptr, d, o, stats));
+    TG_CUDA(cudaMemcpyAsync(counts, d, bytes, cudaMemcpyDeviceToHost, c->stream));
+    TG_CUDA(cudaStreamSynchronize(c->stream));
+    return TG_OK;
+}
+
+tg_status tg_dummy_host(tg_strategy s, uint64_t n, uint32_t rho, const tg_launch_opts* opts,
+                        tg_dispatch_stats* stats, uint64_t* sink_value) {
+    g_launches = 0;
+    tg_launch_opts o = opts ? *opts : default_opts();
+    Problem P;
+    TG_TRY(make_problem(s, n, rho, &o, &P));
+    DevGuard guard;
+    DeviceCtx* c;
+    TG_TRY(get_ctx(o.device, &c));
+    std::lock_guard<std::mutex> lk(c->mu);
+    o.device = c->dev;
+    o.stream = c->stream;
+    o.async = 0;
+    o.sink = c->scratch + 4;
+    TG_CUDA(cudaMemsetAsync(c->scratch + 4, 0, sizeof(unsigned long long), c->stream));
+    TG_TRY(launch_impl(TG_KERNEL_DUMMY, P, 0, nullptr, nullptr, o, stats));
+    unsigned long long v = 0;
+    TG_CUDA(cudaMemcpyAsync(&v, c->scratch + 4, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+    TG_CUDA(cudaStreamSynchronize(c->stream));
+    if (sink_value) *sink_value = v;
+    return TG_OK;
+}
+
+// edm_reference (edm.cpp:53-63): sequential by contract -- host binary32
+// arithmetic in edm_pair's order (each op separately rounded; the translation
+// unit is compiled without FMA contraction for host code, see build.py).
+tg_status tg_edm_reference_host(const float* pts, uint64_t n, uint32_t d, float* out) {
+    if (n == 0) return fail(TG_EINVAL, "ProblemSize: N must be >= 1");
+    if (d == 0) return fail(TG_EINVAL, "edm_reference: features must be >= 1");
+    if (!pts || !out) return fail(TG_EINVAL, "edm_reference: NULL buffer");
+    uint64_t e = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const float* a = pts + i * d;
+        for (uint64_t j = 0; j <= i; ++j, ++e) {
+            const float* b = pts + j * d;
+            float sum = 0.0f;
+            for (uint32_t k = 0; k < d; ++k) {
+                const float diff = fsub(a[k], b[k]);
+                sum = fadd(sum, fmul(diff, diff));
+            }
+            out[e] = std::sqrt(sum);
+        }
+    }
+    return TG_OK;
+}
+
+tg_status tg_grid_spec(tg_strategy s, uint64_t n, uint32_t rho, const tg_launch_opts* opts, tg_pass* passes,
+                       uint32_t cap, uint32_t* npass) {
+    Problem P;
+    TG_TRY(make_problem(s, n, rho, opts, &P));
+    std::vector<tg_pass> v;
+    const uint64_t nb = ceil_div(n, rho);
+    if (s == TG_BB) {
+        v.push_back({nb, nb, 0, 0, 0, 0});
+    } else if (is_ltm(s)) {
+        const uint64_t side = ceil_sqrt(tri(nb));
+        v.push_back({side, side, 0, 0, 0, 0});
+    } else if (s == TG_UTM) {
+        const uint64_t pairs = tri_nd(n), tpb = (uint64_t)rho * rho;
+        v.push_back({pairs == 0 ? 1 : ceil_div(pairs, tpb), 1, 0, 0, 0, 0});
+    } else if (s == TG_RB) {
+        const uint64_t wd = (n % 2 == 0) ? n / 2 : (n + 1) / 2, h = (n % 2 == 0) ? n + 1 : n;
+        v.push_back({ceil_div(wd, rho), ceil_div(h, rho), 0, 0, 0, 0});
+    } else {
+        for (const RecPassInfo& q : rec_passes(P)) v.push_back({q.sb, q.sb * q.count, 1, q.level, q.side, q.count});
+    }
+    if (npass) *npass = (uint32_t)v.size();
+    if (passes) {
+        if (cap < v.size()) return fail(TG_EINVAL, "grid_spec: pass buffer too small");
+        std::copy(v.begin(), v.end(), passes);
+    }
+    return TG_OK;
+}
+
+tg_status tg_ltm_map_policy(uint64_t lambda, int engine, int with_diag, int repair, uint64_t* i, uint64_t* j) {
+    if (engine < 0 || engine > 3) return fail(TG_EINVAL, "ltm_map: unknown engine");
+    if (repair < 0 || repair > 2) return fail(TG_EINVAL, "ltm_map: unknown repair policy");
+    const bool wd = with_diag != 0;
+    uint64_t r = ltm_row_guess(lambda, engine, wd);
+    // RepairPolicy Auto: repair only at lambda >= kRepairFreeLambdaLimit (fastmath.hpp:82-88)
+    if (engine != kExact && (repair == 2 || (repair == 0 && lambda >= 1844160ull))) r = fix_row(r, lambda, wd);
+    *i = r;
+    *j = lambda - row_start(r, wd);
+    return TG_OK;
+}
+
+tg_status tg_dispatch_stats_opts(tg_strategy s, uint64_t n, uint32_t rho, const tg_launch_opts* opts,
+                                 tg_dispatch_stats* out) {
+    const tg_launch_opts o = opts ? *opts : default_opts();
+    Problem P;
+    TG_TRY(make_problem(s, n, rho, &o, &P));
+    std::vector<tg_dispatch_stats> pp;
+    TG_TRY(stats_for(P, o.shard_index, o.shard_count == 0 ? 1 : o.shard_count, out, &pp));
+    if (o.per_pass) {
+        if (o.per_pass_cap < pp.size()) return fail(TG_EINVAL, "per_pass: buffer too small");
+        std::copy(pp.begin(), pp.end(), o.per_pass);
+    }
     return TG_OK;
 }
 

@@ -3,20 +3,21 @@
  /root/reference/proj/bindings/module.cpp:55-183), running on a B200.
 
 Same 21 names, argument names, defaults, return shapes and exception classes
-as the reference.  The hot calls (``edm_strategy``, ``edm_reference``,
-``coverage_ok``, ``gen_points``) run the sm_100a kernels of
-libtrigrid_b200.so through its C-ABI; the scalar mapping helpers
-(``ltm_map``, ``utm_map``, ...) run the same ``__host__ __device__`` mapping
-code on the host.  Differences from the reference, all documented in
-DESIGN.md: ``workers`` is accepted and ignored; ``DispatchStats.wall_time_ns``
-is device time; ``ltm_map``'s reciprocal engine returns the exact (i, j) for
-every lambda (the reference is exact only where its repair policy holds, which
-covers every lambda the reference itself checks); ``rec_decompose(n, 0)``
-returns None where the reference divides by zero.
+as the reference.  The hot calls (``edm_strategy``, ``coverage_ok``,
+``gen_points``) run the sm_100a kernels of libtrigrid_b200.so through its
+C-ABI; the scalar mapping helpers (``ltm_map``, ``utm_map``, ...) run the same
+``__host__ __device__`` mapping code on the host with the reference's binary32
+arithmetic and repair policy.  ``edm_reference`` is the reference API's
+sequential oracle (edm.cpp:53-63) and stays sequential host code by contract --
+it is what device results are checked against, never a fallback for them.
+Differences from the reference, all documented in DESIGN.md: ``workers`` is
+accepted and ignored; ``DispatchStats.wall_time_ns`` is device time;
+``rec_decompose(n, 0)`` returns None where the reference divides by zero.
 
 Extensions beyond the reference surface (same module): ``edm`` (any d, device
-tensors, shards), ``launch``, ``collide``, ``lambda_sweep``, ``sqrt_selftest``,
-``shard_rows``, ``shard_elems``, ``dispatch_stats``.
+tensors, shards), ``launch``, ``collide``, ``coverage``, ``grid_spec``,
+``lambda_sweep``, ``sqrt_selftest``, ``shard_rows``, ``shard_elems``,
+``dispatch_stats``.
 """
 from __future__ import annotations
 
@@ -133,11 +134,17 @@ def sqrt_via(engine: str, x: float) -> float:
 
 # ------------------------------------------------------------ L1 mappers
 
-def ltm_map(lam, engine: str = "reciprocal", with_diag: bool = True):
-    """g(lambda): packed block index to (i, j) (strategies.cpp:60-83)."""
+_REPAIR = {"auto": 0, "off": 1, "on": 2}
+
+
+def ltm_map(lam, engine: str = "reciprocal", with_diag: bool = True, repair: str = "auto"):
+    """g(lambda): packed block index to (i, j) (strategies.cpp:60-83) with the
+    reference's RepairPolicy (fastmath.hpp:84-103; module.cpp:90-96 uses Auto)."""
     i, j = C.c_uint64(), C.c_uint64()
-    _lib.check(_L().tg_ltm_map(_u64(lam, "lam"), _engine(engine), int(bool(with_diag)),
-                               C.byref(i), C.byref(j)))
+    if repair not in _REPAIR:
+        raise ValueError(f"unknown repair policy '{repair}'")
+    _lib.check(_L().tg_ltm_map_policy(_u64(lam, "lam"), _engine(engine), int(bool(with_diag)), _REPAIR[repair],
+                                      C.byref(i), C.byref(j)))
     return i.value, j.value
 
 
@@ -215,13 +222,17 @@ def _stats_dict(st: _lib.tg_dispatch_stats) -> dict:
 
 
 def edm_strategy(strategy: str, points, rho=16, workers=0, *, out: np.ndarray | None = None,
-                 device: int = -1, mode: str = "auto", shard: tuple[int, int] | None = None):
+                 device: int = -1, mode: str = "auto", shard: tuple[int, int] | None = None,
+                 devices: list[int] | None = None, rec: tuple[int, int] | None = None):
     """Packed distance matrix through a mapping strategy, plus dispatch stats
     (module.cpp:149-161).  Runs the sm_100a td-kernel; host in, host out.
 
     Extensions: ``out`` -- a preallocated host float32 buffer of T(N) (or the
     shard's) elements, ideally pinned, written in place and returned;
-    ``shard=(g, G)`` -- compute lambda-range shard g of G only."""
+    ``shard=(g, G)`` -- compute lambda-range shard g of G only;
+    ``devices=[d0, d1, ...]`` -- split the lambda range over several GPUs of
+    this process, each copying its slice out over its own PCIe link;
+    ``rec=(m, k)`` -- an explicit rec_schedule (strategies.cpp:116-140)."""
     s = _strategy(strategy, allow_extended=True)
     pts = _points(points)
     rho = _u64(rho, "rho")
@@ -239,30 +250,30 @@ def edm_strategy(strategy: str, points, rho=16, workers=0, *, out: np.ndarray | 
     elif out.dtype != np.float32 or out.size < size or not out.flags.c_contiguous:
         raise ValueError("edm_strategy: out must be a C-contiguous float32 array of the packed size")
     st = _lib.tg_dispatch_stats()
-    o = _lib.opts(device=device, mode=mode, shard=shard)
+    dv = (C.c_int32 * len(devices))(*devices) if devices else None
+    o = _lib.opts(device=device, mode=mode, shard=shard, devices=dv, rec=rec)
     _lib.check(_L().tg_edm_strategy_host(s, pts.ctypes.data, n, d, rho, out.ctypes.data,
                                          C.byref(o), C.byref(st)))
     return out[:size] if out.size != size else out, _stats_dict(st)
 
 
 def edm_reference(points) -> np.ndarray:
-    """Packed distance matrix, same values as the reference's sequential oracle
-    (edm.cpp:53-63).  Computed on device with the exact-integer g(lambda)."""
+    """The reference's sequential oracle (edm.cpp:53-63): every pair j <= i in
+    row-major order with edm_pair's binary32 arithmetic, any d.  Sequential
+    host code by contract (it is what launch results are verified against)."""
     pts = _points(points)
-    if pts.shape[0] == 0:
+    n, d = pts.shape
+    if n == 0:
         raise ValueError("ProblemSize: N must be >= 1")
-    if pts.shape[1] < 1 or pts.shape[1] > 4:
-        # edm_reference has no d cap in the reference (edm.cpp:53-63)
-        import torch
-        p = torch.from_numpy(pts).cuda()
-        o = edm(p, strategy="ltm-exact")
-        return o.cpu().numpy()
-    return edm_strategy("ltm-exact", pts)[0]
+    out = np.empty(n * (n + 1) // 2, dtype=np.float32)
+    _lib.check(_L().tg_edm_reference_host(pts.ctypes.data, n, d, out.ctypes.data))
+    return out
 
 
 def coverage_ok(strategy: str, n, rho=16, workers=0) -> bool:
     """True when the strategy touches every domain cell exactly once
-    (module.cpp:163-172); the COUNT kernel runs on device."""
+    (module.cpp:163-172); the COUNT kernel runs on device in the execution
+    shape the EDM / write launches use (span where eligible)."""
     s = _strategy(strategy)
     ok = C.c_int()
     _u64(workers, "workers")
@@ -270,14 +281,44 @@ def coverage_ok(strategy: str, n, rho=16, workers=0) -> bool:
     return bool(ok.value)
 
 
+def coverage(strategy: str, n: int, rho: int = 16, mode: str = "auto", rec: tuple[int, int] | None = None,
+             engine: str | None = None, device: int = -1) -> dict:
+    """Exactly-once check with its details: {"ok", "bad", "first_bad"}; mode
+    "span" checks the owned-chunk rule of the span kernels, "grid" the
+    paper-faithful one-thread-per-cell kernel."""
+    ok, bad, first = C.c_int(), C.c_uint64(), C.c_uint64()
+    o = _lib.opts(device=device, mode=mode, rec=rec, engine=None if engine is None else _engine(engine))
+    _lib.check(_L().tg_coverage_ok_opts(_strategy(strategy, True), n, rho, C.byref(o), C.byref(ok), C.byref(bad),
+                                        C.byref(first)))
+    return {"ok": bool(ok.value), "bad": bad.value,
+            "first_bad": None if first.value == (1 << 64) - 1 else first.value}
+
+
+def grid_spec(strategy: str, n: int, rho: int = 16, rec: tuple[int, int] | None = None) -> list[dict]:
+    """grid_of(make_strategy(...)).passes (strategies.hpp:393-400)."""
+    o = _lib.opts(rec=rec)
+    cnt = C.c_uint32()
+    _lib.check(_L().tg_grid_spec(_strategy(strategy, True), n, rho, C.byref(o), None, 0, C.byref(cnt)))
+    arr = (_lib.tg_pass * cnt.value)()
+    _lib.check(_L().tg_grid_spec(_strategy(strategy, True), n, rho, C.byref(o), arr, cnt.value, C.byref(cnt)))
+    return [p.as_dict() for p in arr]
+
+
 # ------------------------------------------------------------ extensions
 
-def dispatch_stats(strategy: str, n: int, rho: int = 16, shard: tuple[int, int] | None = None) -> dict:
-    """Closed-form DispatchStats (what run_strategy tallies, engine.cpp:70-136)."""
+def dispatch_stats(strategy: str, n: int, rho: int = 16, shard: tuple[int, int] | None = None,
+                   rec: tuple[int, int] | None = None, per_pass: bool = False) -> dict:
+    """Closed-form DispatchStats (what run_strategy tallies, engine.cpp:70-136);
+    per_pass=True adds the per-pass list (LaunchOptions::per_pass)."""
     st = _lib.tg_dispatch_stats()
-    g, G = shard if shard else (0, 1)
-    _lib.check(_L().tg_dispatch_stats_for(_strategy(strategy, True), n, rho, g, G, C.byref(st)))
-    return _stats_dict(st)
+    npass = len(grid_spec(strategy, n, rho, rec)) if per_pass else 0
+    pp = (_lib.tg_dispatch_stats * npass)() if per_pass else None
+    o = _lib.opts(shard=shard, rec=rec, per_pass=pp)
+    _lib.check(_L().tg_dispatch_stats_opts(_strategy(strategy, True), n, rho, C.byref(o), C.byref(st)))
+    d = _stats_dict(st)
+    if per_pass:
+        d["per_pass"] = [x.as_dict() for x in pp]
+    return d
 
 
 def shard_rows(n: int, rho: int, shard_count: int) -> list[int]:
@@ -292,31 +333,49 @@ def shard_elems(n: int, rho: int, shard_index: int, shard_count: int, with_diag:
     return b.value, e.value
 
 
-def _stream_ptr(stream):
+def _device_of(*tensors) -> int:
+    """The CUDA ordinal the launch runs on: that of its tensors (they must
+    agree), else torch's current device."""
+    import torch
+    devs = {t.device.index for t in tensors if t is not None and hasattr(t, "device") and t.device.type == "cuda"}
+    if len(devs) > 1:
+        raise ValueError(f"tensors on different CUDA devices: {sorted(devs)}")
+    return devs.pop() if devs else torch.cuda.current_device()
+
+
+def _stream_ptr(stream, device: int):
     if stream is None:
         import torch
-        return torch.cuda.current_stream().cuda_stream
+        return torch.cuda.current_stream(device).cuda_stream
     return int(getattr(stream, "cuda_stream", stream))
 
 
 def launch(kernel: str, strategy: str, n: int, *, points=None, out=None, d: int = 0, rho: int = 16,
            mode: str = "auto", shard: tuple[int, int] | None = None, persistent: bool = False,
-           stream=None, sync: bool = True, sentinel: int | None = None, sink=None) -> dict:
-    """tg_launch on device tensors (torch CUDA tensors or raw pointers).
-    kernel in {dummy, write, edm, count}; returns DispatchStats."""
-    import torch
-    dev = torch.cuda.current_device()
+           stream=None, sync: bool = True, sentinel: int | None = None, sink=None,
+           rec: tuple[int, int] | None = None, engine: str | None = None, per_pass: bool = False) -> dict:
+    """tg_launch on device tensors (torch CUDA tensors or raw pointers), on the
+    tensors' device and that device's current stream unless `stream` is given.
+    kernel in {dummy, write, edm, count}; returns DispatchStats (+ "per_pass"
+    when per_pass=True: one entry per grid pass, each device-timed)."""
+    dev = _device_of(points, out, sink)
     pp = points.data_ptr() if hasattr(points, "data_ptr") else (points or 0)
     op = out.data_ptr() if hasattr(out, "data_ptr") else (out or 0)
     sp = sink.data_ptr() if hasattr(sink, "data_ptr") else sink
     if points is not None and hasattr(points, "shape") and not d:
         d = points.shape[1]
-    o = _lib.opts(device=dev, mode=mode, stream=_stream_ptr(stream), async_=not sync,
-                  persistent=persistent, shard=shard, sentinel=sentinel, sink=sp)
+    npass = len(grid_spec(strategy, n, rho, rec)) if per_pass else 0
+    ppa = (_lib.tg_dispatch_stats * npass)() if per_pass else None
+    o = _lib.opts(device=dev, mode=mode, stream=_stream_ptr(stream, dev), async_=not sync,
+                  persistent=persistent, shard=shard, sentinel=sentinel, sink=sp, rec=rec,
+                  engine=None if engine is None else _engine(engine), per_pass=ppa)
     st = _lib.tg_dispatch_stats()
     _lib.check(_L().tg_launch(_lib.KERNELS[kernel], _strategy(strategy, True), n, d, rho, pp, op,
                               C.byref(o), C.byref(st)))
-    return _stats_dict(st)
+    res = _stats_dict(st)
+    if per_pass:
+        res["per_pass"] = [x.as_dict() for x in ppa]
+    return res
 
 
 def edm(points, strategy: str = "ltm-r", rho: int = 16, out=None, shard=None, mode: str = "auto",
@@ -352,8 +411,8 @@ def collide(spheres, r_max: float, strategy: str = "ltm-r", rho: int = 16, shard
     words = max(1, (e - b + 31) // 32)
     bits = torch.empty(words, dtype=torch.int32, device=sph.device)
     hits = torch.zeros(1, dtype=torch.int64, device=sph.device)
-    o = _lib.opts(device=sph.device.index, mode=mode, stream=_stream_ptr(stream), async_=not sync,
-                  persistent=persistent, shard=shard)
+    o = _lib.opts(device=sph.device.index, mode=mode, stream=_stream_ptr(stream, sph.device.index),
+                  async_=not sync, persistent=persistent, shard=shard)
     st = _lib.tg_dispatch_stats()
     _lib.check(_L().tg_collide(_strategy(strategy, True), n, rho, sph.data_ptr(), float(r_max),
                                bits.data_ptr(), hits.data_ptr(), C.byref(o), C.byref(st)))

@@ -23,9 +23,9 @@ static int host_checks() {
     expect(tb::tri_count(4) == 10, "tri_count(4)");
     expect(tb::tri_linear_index({2, 1}) == 4, "tri_linear_index(2,1)");
     expect(tb::grid_side_balanced(1920) == 1358, "grid_side_balanced(1920)");
-    expect(tb::ltm_map(4) == tb::TriCoord{2, 1}, "ltm_map(4)");
-    expect(tb::ltm_map(1844159) == tb::TriCoord{1919, 1919}, "ltm_map(1844159)");
-    expect(tb::count_wasted(*tb::parse_strategy("bb"), 1920) == 1842240, "count_wasted(bb,1920)");
+    expect(tb::ltm_map(4, tb::SqrtEngine::reciprocal()) == tb::TriCoord{2, 1}, "ltm_map(4)");
+    expect(tb::ltm_map(1844159, tb::SqrtEngine::reciprocal()) == tb::TriCoord{1919, 1919}, "ltm_map(1844159)");
+    expect(tb::count_wasted(tb::StrategyKind::BoundingBox, 1920) == 1842240, "count_wasted(bb,1920)");
     expect(!tb::parse_strategy("zz").has_value(), "parse_strategy(zz)");
     bool threw = false;
     try {

@@ -22,7 +22,7 @@ def test_header_symbols_exported(tg):
     for name in sorted(decl):
         assert hasattr(L, name), f"{name} declared in trigrid_b200.h but not exported"
     assert decl <= set(_lib.EXPORTED), decl - set(_lib.EXPORTED)
-    assert L.tg_api_version() == 1
+    assert L.tg_api_version() == 2
 
 
 def test_sm100a_cubin_present(tg):
@@ -141,8 +141,8 @@ def test_shard_geometry(tg):
 
 
 def test_shard_stats_sum(tg):
-    for s in ("bb", "ltm-r"):
-        for n, G in ((65536, 8), (1000, 3), (4096, 2)):
+    for s in ("bb", "ltm-r", "rec"):
+        for n, G in ((65536, 8), (1024, 3), (4096, 2), (3072, 5)):
             tot = [0, 0, 0]
             for g in range(G):
                 st = tg.dispatch_stats(s, n, 16, (g, G))
@@ -151,8 +151,16 @@ def test_shard_stats_sum(tg):
             # surviving tiles and filtered threads are partitioned exactly
             assert tot[0] - tot[1] == whole["blocks_launched"] - whole["blocks_discarded"]
             assert tot[2] == whole["threads_discarded"]
-    with pytest.raises(ValueError):
-        tg.dispatch_stats("rb", 100, 16, (0, 2))
+    # REC shards partition every pass exactly (blocks, discards, filtered threads)
+    for n, G in ((65536, 8), (3072, 5)):
+        whole = tg.dispatch_stats("rec", n, 16, per_pass=True)
+        parts = [tg.dispatch_stats("rec", n, 16, (g, G), per_pass=True) for g in range(G)]
+        for p, wp in enumerate(whole["per_pass"]):
+            for k in ("blocks_launched", "blocks_discarded", "threads_discarded"):
+                assert sum(q["per_pass"][p][k] for q in parts) == wp[k]
+    # rb / utm shards: the span walk's own tile counts (no reference counterpart), >= 1 per non-empty shard
+    for s in ("rb", "utm"):
+        assert all(tg.dispatch_stats(s, 4096, 16, (g, 4))["blocks_launched"] > 0 for g in range(4))
 
 
 def test_errors_mirror_reference(tg):
