@@ -121,6 +121,49 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
+# ------------------------------------------------------------------ verify
+
+def golden_sha(n: int, d: int, rank: int, world: int):
+    """The reference's sha256 of this rank's packed slice (tests/golden/
+    golden_large.json, generated from oracle/_ref = the unmodified reference
+    build; the GPU box has no /root/reference), or None if not recorded."""
+    p = os.path.join(ROOT, "tests", "golden", "golden_large.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        g = json.load(f)
+    if world == 1:
+        return g.get("edm", {}).get(f"{n}|{d}", {}).get("sha256")
+    sh = g.get("edm_shards", {}).get(f"{n}|{d}", {}).get(str(world))
+    return sh["sha256"][rank] if sh else None
+
+
+def sha256_device(t, chunk_bytes: int = 1 << 28) -> str:
+    """sha256 of a CUDA tensor's bytes through a pinned staging buffer
+    (outside every timed region)."""
+    import hashlib
+
+    import torch
+    flat = t.reshape(-1).view(torch.uint8)
+    h = hashlib.sha256()
+    stage = torch.empty(min(chunk_bytes, flat.numel()), dtype=torch.uint8).pin_memory()
+    for a in range(0, flat.numel(), chunk_bytes):
+        m = min(chunk_bytes, flat.numel() - a)
+        stage[:m].copy_(flat[a:a + m])
+        h.update(memoryview(stage[:m].numpy()))
+    return h.hexdigest()
+
+
+def sha256_host(a) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    mv = memoryview(a.reshape(-1).view("u1"))
+    step = 1 << 28
+    for i in range(0, len(mv), step):
+        h.update(mv[i:i + step])
+    return h.hexdigest()
+
+
 # ------------------------------------------------------------ reference arm
 
 def cpu_reference_run(n: int, d: int, strategy: str, steps: int, warmup: int, budget_s: float | None):
@@ -189,7 +232,6 @@ def run_reference(args):
 # ------------------------------------------------------------------ our arm
 
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -309,7 +351,7 @@ def run_ours(args):
         wbuf = out.view(torch.int32)
         pm_steps, pm_warm = 5, 2
         rows = {}
-        span_strats = ["bb", "ltm-r", "ltm-n", "ltm-x", "ltm-exact"] + (["rec"] if world == 1 else [])
+        span_strats = ["bb", "ltm-r", "ltm-n", "ltm-x", "ltm-exact", "rec", "rb", "utm"]
         for s in span_strats:
             e_ms = time_steps(lambda: step(strat=s), pm_steps, pm_warm)
             w_ms = time_steps(lambda: step(strat=s, kernel="write", o=wbuf), pm_steps, pm_warm)
@@ -428,8 +470,21 @@ def run_ours(args):
            "path": "trigrid.edm_strategy(host pinned) -> tg_edm_strategy_host (C-ABI): H2D points, "
                    "kernel in block-row pieces, D2H pipelined per piece",
            "d2h_gbs_per_rank": 4 * cells_local / sec / 1e9}
-    check_row = int(np.random.default_rng(0).integers(0, n))
     clk = clocks.stop()
+
+    # ---- verify what was timed (outside every timed region): the headline
+    # buffer and the e2e host buffer against the reference's sha256
+    want = golden_sha(n, d, rank, world)
+    step()
+    torch.cuda.synchronize(dev)
+    got_dev = sha256_device(out)
+    got_host = sha256_host(host_out)
+    verify = {"golden": "tests/golden/golden_large.json (reference launch_edm, oracle/_ref)",
+              "want_sha256": want, "device_sha256": got_dev, "e2e_host_sha256": got_host,
+              "ok": bool(want) and got_dev == want and got_host == want,
+              "bytes": 4 * cells_local, "shard": [rank, world]}
+    if not want:
+        verify["note"] = f"no golden sha recorded for n={n} d={d} shards={world}"
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -437,6 +492,16 @@ def run_ours(args):
         try:
             r = cpu_reference_run(n, d, strategy, 3, 1, args.cpu_budget)
             cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            if not args.quick:
+                # the reference's own launch_edm per mapping (bench.cpp:86-96), one timed call each
+                pm = {}
+                for s in ("bb", "ltm-r", "rb", "rec", "utm"):
+                    rs = cpu_reference_run(n, d, s, 1, 0, None)
+                    pm[s] = {"value": rs["value"], "ms_per_step": rs["ms_per_step"], "kind": rs["kind"],
+                             "cores": rs["cores"]}
+                for s, r_ in pm.items():
+                    r_["I_vs_bb"] = pm["bb"]["ms_per_step"] / r_["ms_per_step"]
+                cpu["per_mapping"] = pm
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
 
@@ -451,7 +516,7 @@ def run_ours(args):
         "gpu_launches": launches_per_step * args.steps,
         "per_mapping": per_mapping,
         "other_configs": other,
-        "verify": {"row": check_row},
+        "verify": verify,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

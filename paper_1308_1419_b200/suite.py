@@ -105,7 +105,9 @@ def run_suite(cfg: BenchConfig) -> SuiteResult:
         reference = None
         verify_here = edm and n <= cfg.verify_cap
         if verify_here:
-            reference = tg.edm(pts, strategy="ltm-exact", rho=cfg.rho).clone()
+            # edm_reference (edm.cpp:53-63): the sequential host restatement of the reference API,
+            # independent of every device kernel -- as run_suite verifies (bench.cpp:100-108)
+            reference = torch.from_numpy(tg.edm_reference(pts.cpu().numpy())).to(dev)
 
         def launch_once(s):
             if cfg.kernel == "dummy":
