@@ -65,8 +65,8 @@ typedef enum {
 
 /* Execution mode. */
 typedef enum {
-    TG_MODE_AUTO = 0, /* span when the strategy/rho/body allow it (bb, ltm-*, rec, rb: rho % 4 == 0;
-                         utm: rho a power of two in [4, 128]; bodies edm d <= 4, write, count;
+    TG_MODE_AUTO = 0, /* span when the strategy/rho/body allow it (every strategy: rho % 4 == 0,
+                         rho <= 128; bodies edm d <= 4, write, count;
                          d > 4 and collide: bb, ltm-*, rec), else grid */
     TG_MODE_GRID = 1, /* paper-faithful: one CTA of rho*rho threads per grid block, one cell per thread */
     TG_MODE_SPAN = 2, /* B200: warp per run of consecutive blocks, 128-bit owned-chunk stores */

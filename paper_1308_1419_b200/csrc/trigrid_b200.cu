@@ -421,23 +421,22 @@ int span_slots() {
     return p;
 }
 
-bool pow2(uint64_t v) { return v && !(v & (v - 1)); }
 
-// Strategies / rho with a span form: row tiles for bb, ltm-*, rec, rb
-// (rho % 4 == 0); column runs for utm (rho / 4 must divide 32).
+// Strategies / rho with a span form (row tiles; utm: super-block slabs):
+// every strategy with rho % 4 == 0.
 bool span_eligible(tg_strategy s, uint32_t rho) {
-    if (s == TG_UTM) return pow2(rho) && rho >= 4 && rho <= 128;
-    return (s == TG_BB || is_ltm(s) || s == TG_REC || s == TG_RB) && rho % 4 == 0 && rho <= 128;
+    (void)s;
+    return rho % 4 == 0 && rho <= 128;
 }
 // Bodies restricted to the square-tile strategies (16-row tiles at block-row
 // multiples: the d > 4 kernels, the collision kernel).
 bool square_tiles(tg_strategy s) { return s == TG_BB || is_ltm(s) || s == TG_REC; }
 
-// UTM grid blocks per unit (column run of C rho-row blocks).  A/B: TG_UTM_C.
-uint32_t utm_blocks_per_unit() {
-    static uint32_t v = [] {
-        const char* e = std::getenv("TG_UTM_C");
-        return e ? (uint32_t)std::max(1, std::atoi(e)) : 8u;
+// UTM super-block side in run widths.  A/B: TG_UTM_RUNS.
+uint64_t utm_runs() {
+    static uint64_t v = [] {
+        const char* e = std::getenv("TG_UTM_RUNS");
+        return e ? (uint64_t)std::max(1, std::atoi(e)) : 16ull;
     }();
     return v;
 }
@@ -531,19 +530,32 @@ tg_status plan_span_c(const Problem& P, const Window& w, uint32_t C, SpanGeom* g
         uint64_t y[4];
         rb_row_ranges(P, w, y);
         uint64_t unit = 0;
-        add_pass(g, unit, y[0], y[1], ceil_div(wd, rho), 0, 0, C);  // direct part
-        add_pass(g, unit, y[2], y[3], ceil_div(wd, rho), 0, 1, C);  // folded part
+        if (y[0] < y[3] && y[2] < y[1]) {
+            // the direct and folded rect-row ranges overlap (always for the whole
+            // domain): one pass over their union, each unit emitting both of its
+            // complementary parts (clipped to the window), so no unit is empty
+            add_pass(g, unit, std::min(y[0], y[2]), std::max(y[1], y[3]), ceil_div(wd, rho), 0, 2, C);
+        } else {
+            add_pass(g, unit, y[0], y[1], ceil_div(wd, rho), 0, 0, C);  // direct part
+            add_pass(g, unit, y[2], y[3], ceil_div(wd, rho), 0, 1, C);  // folded part
+        }
         g->units = unit;
     } else if (s == TG_UTM) {
         g->strat = kSpanUTM;
         g->engine = P.engine;
-        g->C = utm_blocks_per_unit();
-        g->H = b1 - b0;
-        g->rect_blocks = b0 * g->H;
-        g->u_rect = ceil_div(g->rect_blocks, g->C);
-        g->tri_blocks = tri(g->H);  // = T_nodiag(H + 1) pairs of the block-level UTM
+        // super-blocks of W = utm_runs() run widths (C rho columns each); one
+        // unit per 16-row x run tile
+        const uint64_t runs = utm_runs(), S = (uint64_t)C * rho * runs, R0 = std::min(n, b0 * rho);
+        const uint64_t He = w.r_hi - R0;
+        g->W = S;
+        g->ur = runs;
+        g->H = ceil_div(He, S);
+        g->rect_blocks = ceil_div(He, 16) * runs;  // units per rectangle strip
+        g->u_rect = ceil_div(R0, S) * g->rect_blocks;
+        g->upb = ceil_div(S, 16) * runs;
+        g->tri_blocks = tri(g->H);  // = T_nodiag(H + 1) pairs of the super-block-level UTM
         g->disc = (2 * g->H + 1) * (2 * g->H + 1);
-        g->units = g->u_rect + ceil_div(g->tri_blocks, g->C);
+        g->units = g->u_rect + g->tri_blocks * g->upb;
     } else {
         return fail(TG_EINVAL, "span mode: unknown strategy");
     }
@@ -1025,9 +1037,8 @@ tg_status launch_impl(tg_kernel kernel, const Problem& P, uint32_t d, const floa
                            (kernel == TG_KERNEL_DUMMY && o.mode == TG_MODE_SPAN);
     const bool span = resolve_span(o, s, rho, body_span);
     if (span && !(body_span && span_eligible(s, rho)))
-        return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec/rb (rho % 4 == 0) or utm (rho a power of two in "
-                               "[4, 128]) and an edm (d <= 4; d > 4 with rho == 16 for bb/ltm-*/rec), write, "
-                               "count or dummy body");
+        return fail(TG_EINVAL, "span mode needs rho % 4 == 0, rho <= 128 and an edm (d <= 4; d > 4 with "
+                               "rho == 16 for bb/ltm-*/rec), write, count or dummy body");
     if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode");
 
     const bool timed_passes = o.per_pass && !o.async && pp.size() > 1;
@@ -1370,7 +1381,7 @@ tg_status edm_host_shard(const Problem& P, const float* pts, uint32_t d, float* 
     const bool span = resolve_span(o, P.s, rho, true);
     if (G > 1 && !span) return fail(TG_EINVAL, "sharded launches run in span mode");
     if (span && !span_eligible(P.s, rho))
-        return fail(TG_EINVAL, "span mode needs bb/ltm-*/rec/rb (rho % 4 == 0) or utm (rho a power of two)");
+        return fail(TG_EINVAL, "span mode needs rho % 4 == 0 and rho <= 128");
     const Window w = window_of(P, shard, G);
     const uint64_t b0 = w.b0, b1 = w.b1;
     const uint64_t eb = tri(w.r_lo), ee = tri(w.r_hi);
