@@ -72,7 +72,9 @@ typedef enum {
     TG_MODE_SPAN = 2, /* B200: warp per run of consecutive blocks, 128-bit owned-chunk stores */
     TG_MODE_GRAM = 3  /* EDM only: Gram trick on tcgen05 (fp16 hi/lo split, kind::f16, any d),
                          stated tolerance
-                         |d^2 - d_exact^2| <= 2^-17 (|x_i|^2 + |x_j|^2), diagonal 0; not bit-exact */
+                         |d^2 - d_exact^2| <= 2^-17 (|x_i|^2 + |x_j|^2), diagonal 0; not bit-exact.
+                         Any magnitude spread: one power-of-two operand scale when the per-point
+                         max |x| spans <= 2^20, per-point scales beyond (finite inputs) */
 } tg_mode;
 
 /* Mirrors trigrid::DispatchStats field for field (engine.hpp:19-32).

@@ -334,8 +334,9 @@ constexpr uint32_t kG2TmemCols = 512;
 constexpr int kG2QChunks = 33;                // quarter staging row stride in chunks (32 used, odd: no conflicts)
 constexpr uint32_t kG2EpiBytes = 32 * kG2QChunks * 16 / (kG2EpiWarps / 4);  // per epilogue warp
 constexpr uint32_t kG2NormSlots = 8;          // norm ring: [column norms 136 | pad | row norms 128] floats
-constexpr uint32_t kG2NormSlot = (136 + 8 + 128) * 4;
+constexpr uint32_t kG2NormSlot = 2 * (136 + 8 + 128) * 4;  // norms | per-point scale factors (wide range)
 constexpr uint32_t kG2NormRowOff = (136 + 8) * 4;
+constexpr uint32_t kG2FacOff = (136 + 8 + 128) * 4;
 // kind::f16 (A, B fp16, K-major), fp32 accumulate, M = 128, N = 136
 constexpr uint32_t kG2Idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((kG2N >> 3) << 17) |
                               ((uint32_t)(kGT >> 4) << 24);
@@ -425,12 +426,35 @@ __device__ __forceinline__ void g2_commit(uint32_t bar) {
 __device__ __forceinline__ void g2_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void g2_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+#ifndef TG_G2_L2
+#define TG_G2_L2 0  // 1: operands bulk-loaded with an L2 evict_last policy, packed output stored .cs (evict first)
+#endif
+// one bulk global -> shared copy completing on `bar`; pol = an L2 cache
+// policy (TG_G2_L2) or ignored
+__device__ __forceinline__ void g2_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+#if TG_G2_L2
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+#else
+    (void)pol;
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
         "l"(src), "r"(bytes), "r"(bar)
         : "memory");
+#endif
+}
+
+__device__ __forceinline__ void g2_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void g2_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                             uint64_t pol = 0) {
+    g2_expect(bar, bytes);
+    g2_copy(dst, src, bytes, bar, pol);
 }
 
 // next tile of the g(lambda) order: (i, j) -> (i, j + 1), row end -> (i + 1, 0)
@@ -480,24 +504,37 @@ __device__ __forceinline__ void g2_ld32(uint32_t taddr, uint32_t* v) {
         : "r"(taddr));
 }
 
-// Pass 1: |x_i|^2 (fp32 sequential fma, 0 for padding rows) and max |x|.
+// Pass 1: |x_i|^2 (fp32 sequential fma, 0 for padding rows), the point's
+// max |x| (pmax, binary32 bits) and over all points bits[0] = max |x|,
+// bits[1] = ~(smallest nonzero per-point max |x|) (atomicMax of the complement).
 __global__ void gram_prep_kernel(const float* __restrict__ pts, uint64_t n, uint64_t n_pad, uint32_t d,
-                                 float* __restrict__ norms, unsigned int* __restrict__ maxbits) {
-    unsigned int mb = 0;
+                                 float* __restrict__ norms, unsigned int* __restrict__ pmax,
+                                 unsigned int* __restrict__ bits) {
+    unsigned int mb = 0, mn = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad;
          i += (uint64_t)gridDim.x * blockDim.x) {
         float s = 0.0f;
+        unsigned int pm = 0;
         if (i < n) {
             for (uint32_t k = 0; k < d; ++k) {
                 const float a = __ldg(pts + i * d + k);
                 s = fmaf(a, a, s);
-                mb = max(mb, __float_as_uint(a) & 0x7fffffffu);
+                pm = max(pm, __float_as_uint(a) & 0x7fffffffu);
             }
         }
         norms[i] = s;
+        pmax[i] = pm;
+        mb = max(mb, pm);
+        if (pm) mn = max(mn, ~pm);
     }
-    for (int o = 16; o; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
-    if ((threadIdx.x & 31) == 0 && mb) atomicMax(maxbits, mb);
+    for (int o = 16; o; o >>= 1) {
+        mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+        mn = max(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (mb) atomicMax(bits, mb);
+        if (mn) atomicMax(bits + 1, mn);
+    }
 }
 
 // power-of-two exponent s with max|x| * 2^s in [2^14, 2^15), clamped to
@@ -508,6 +545,19 @@ __device__ __forceinline__ int g2_scale_exp(unsigned int maxbits) {
     return max(-63, min(63, 14 - e));
 }
 
+// Wide dynamic range: one global scale puts max|x| at 2^14; a
+// point whose own max|x| is 2^20 x smaller has its hi/lo pair near fp16's
+// subnormal floor and the tolerance no longer holds for its pairs (CPU
+// emulation: err/bound 0.2 at a 1e7 magnitude ratio, 2.6 at 1e8).  Beyond a
+// 2^20 spread of per-point max|x| every point gets its own power-of-two scale
+// s_i (same [2^14, 2^15) placement) and the epilogue unscales each product by
+// 2^-s_i 2^-s_j (row factor per lane, column factors through the norm ring).
+__device__ __forceinline__ bool g2_wide_range(const unsigned int* bits) {
+    const unsigned int mx = __ldg(bits), mn = ~__ldg(bits + 1);
+    if (mx == 0 || __ldg(bits + 1) == 0) return false;
+    return (int)(mx >> 23) - (int)(mn >> 23) > 20;
+}
+
 // Pass 2: x * 2^s = hi + lo in fp16, in the UMMA layout (8-point x 16-byte
 // core matrices, K-major).  Row-tile operand opA: block (tile t, slice k) at
 // (t * nk + k) * 32 KB (hi | lo), points permuted by g2_perm_inv.  Column
@@ -515,9 +565,12 @@ __device__ __forceinline__ int g2_scale_exp(unsigned int maxbits) {
 // (hi array, then lo array, g.bslice bytes each, one zero group past the last
 // tile).  One thread per (point, 8-feature group); padding is zero.
 __global__ void gram_split_kernel(const float* __restrict__ pts, uint64_t n, uint64_t n_pad, uint32_t d,
-                                  uint32_t nk, const unsigned int* __restrict__ maxbits, uint8_t* __restrict__ opA,
-                                  uint8_t* __restrict__ opB, uint64_t bslice) {
-    const float sc = exp2f((float)g2_scale_exp(__ldg(maxbits)));
+                                  uint32_t nk, const unsigned int* __restrict__ bits,
+                                  const unsigned int* __restrict__ pmax, float* __restrict__ facs,
+                                  uint8_t* __restrict__ opA, uint8_t* __restrict__ opB, uint64_t bslice) {
+    const bool wide = g2_wide_range(bits);
+    const int sg = g2_scale_exp(__ldg(bits));
+    const float scg = exp2f((float)sg);
     const uint32_t groups = nk * 8;
     const uint64_t total = (n_pad + 8) * groups;
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < total;
@@ -525,6 +578,12 @@ __global__ void gram_split_kernel(const float* __restrict__ pts, uint64_t n, uin
         const uint64_t row = v / groups;
         const uint32_t g = (uint32_t)(v % groups);
         const uint32_t k0 = 8 * g;
+        float sc = scg;
+        if (wide) {  // per-point scale, its unscale factor 2^-s_i for the epilogue
+            const int si = g2_scale_exp(__ldg(pmax + row));
+            sc = exp2f((float)si);
+            if (g == 0) facs[row] = exp2f((float)-si);
+        }
         __half hi[8], lo[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
@@ -559,30 +618,67 @@ __device__ __forceinline__ void g2_ld8(uint32_t taddr, uint32_t* v) {
                  : "r"(taddr));
 }
 
+#ifndef TG_G2_SQRT
+#define TG_G2_SQRT 0  // epilogue sqrt: 0 MUFU.SQRT, 1 FMA-pipe (magic seed + 2 steps), 2 half and half
+#endif
+
+// sqrt of two non-negative floats on the FMA pipe (no MUFU, i.e. no MIO
+// slot): inverse-sqrt seed 0x5F1FFFF9 - (bits >> 1) with the one-step
+// correction of Moroz et al. (max rel. error 6.5e-4), one Newton step, then
+// x * y.  x = 0 gives 0 (finite seed).  Max relative error of d 7.7e-7
+// (2^-20.3, binary32 emulation over all exponents), i.e. <= 2^-18.3
+// (|x_i|^2 + |x_j|^2) on d^2 -- inside the stated Gram tolerance together
+// with the split error (measured <= 0.11 of it).
+__device__ __forceinline__ float2 g2_sqrt2_fma(float2 x) {
+    float2 y = make_float2(__uint_as_float(0x5F1FFFF9u - (__float_as_uint(x.x) >> 1)),
+                           __uint_as_float(0x5F1FFFF9u - (__float_as_uint(x.y) >> 1)));
+    float2 t = __fmul2_rn(__fmul2_rn(x, y), y);
+    t = __ffma2_rn(t, make_float2(-0.703952253f, -0.703952253f), make_float2(1.681914091f, 1.681914091f));
+    y = __fmul2_rn(y, t);
+    const float2 xy = __fmul2_rn(x, y);
+    t = __ffma2_rn(__fmul2_rn(xy, y), make_float2(-0.5f, -0.5f), make_float2(1.5f, 1.5f));
+    return __fmul2_rn(xy, t);
+}
+
 // d for the 32 owned columns S .. S+31 of the loaded 40 (S = warp-uniform
 // shift): d^2 = |x_i|^2 + |x_j|^2 - 2 * 2^-2s * acc, clamped at 0, sqrt.approx.
 // nb4 = the 16-byte aligned column norms of loaded columns 0 .. 39 (broadcast).
-template <int S, int SV = S>
-__device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, float ni, float m2, float* dv) {
+// WIDE: per-point scales -- acc is first multiplied by the column factors
+// 2^-s_j (cb4, same layout as nb4) and m2 = -2 * 2^-s_i is the row's.
+template <int S, int SV = S, bool WIDE = false>
+__device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, const float4* cb4, float ni, float m2,
+                                       float* dv) {
     const float2 m22 = make_float2(m2, m2), ni2 = make_float2(ni, ni);
-    float4 lo = nb4[0];
+    float4 lo = nb4[0], clo = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (WIDE) clo = cb4[0];
 #pragma unroll
     for (int c4 = 0; c4 < 8; ++c4) {
         const float4 hi = nb4[c4 + 1];
         const float w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};  // columns 4 c4 .. 4 c4 + 7
+        float4 chi = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (WIDE) chi = cb4[c4 + 1];
+        const float cw[8] = {clo.x, clo.y, clo.z, clo.w, chi.x, chi.y, chi.z, chi.w};
 #pragma unroll
         for (int t = 0; t < 4; t += 2) {
             const int p = 4 * c4 + t;
-            const float2 acc = make_float2(__uint_as_float(v[SV + p]), __uint_as_float(v[SV + p + 1]));
+            float2 acc = make_float2(__uint_as_float(v[SV + p]), __uint_as_float(v[SV + p + 1]));
+            if (WIDE) acc = __fmul2_rn(acc, make_float2(cw[S + t], cw[S + t + 1]));
             const float2 nn = __fadd2_rn(ni2, make_float2(w[S + t], w[S + t + 1]));
             const float2 d2 = __ffma2_rn(acc, m22, nn);
             float d0, d1;
-            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(fmaxf(d2.x, 0.0f)));
-            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(fmaxf(d2.y, 0.0f)));
+            if (TG_G2_SQRT == 1 || (TG_G2_SQRT == 2 && (t & 2))) {
+                const float2 r = g2_sqrt2_fma(make_float2(fmaxf(d2.x, 0.0f), fmaxf(d2.y, 0.0f)));
+                d0 = r.x;
+                d1 = r.y;
+            } else {
+                asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(fmaxf(d2.x, 0.0f)));
+                asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(fmaxf(d2.y, 0.0f)));
+            }
             dv[p] = d0;
             dv[p + 1] = d1;
         }
         lo = hi;
+        if (WIDE) clo = chi;
     }
 }
 
@@ -591,19 +687,22 @@ __device__ __forceinline__ void g2_bar_quarter(uint32_t q) {
     asm volatile("bar.sync %0, %1;" ::"r"(q + 1), "n"(32 * (kG2EpiWarps / 4)) : "memory");
 }
 
-__device__ __forceinline__ float g2_dist(uint32_t accbits, float ni, float nj, float m2) {
+__device__ __forceinline__ float g2_dist(uint32_t accbits, float ni, float nj, float m2, float cj = 1.0f) {
     float dd;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(dd) : "f"(fmaxf(fmaf(__uint_as_float(accbits), m2, __fadd_rn(ni, nj)), 0.0f)));
+    const float acc = __fmul_rn(__uint_as_float(accbits), cj);
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(dd) : "f"(fmaxf(fmaf(acc, m2, __fadd_rn(ni, nj)), 0.0f)));
     return dd;
 }
 
 __global__ void __launch_bounds__(kG2Threads, 1)
     gram2_edm_kernel(const __grid_constant__ Gram2Geom g, const uint8_t* __restrict__ opA,
                      const uint8_t* __restrict__ opB, const float* __restrict__ norms,
-                     const unsigned int* __restrict__ maxbits, float* __restrict__ out) {
+                     const float* __restrict__ facs, const unsigned int* __restrict__ bits,
+                     float* __restrict__ out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t nk = g.nk, R = g.ring;
     const bool as = g.a_stream != 0;
+    const bool wide = g2_wide_range(bits);  // per-point scales (uniform across the grid)
     uint8_t* sA = smem;                                   // resident row tile: nk x 32 KB (MMA A)
     uint8_t* sB = smem + (as ? 0u : nk * kG2Slice);       // ring: R x ([row slice 32 KB] | col hi | col lo)
     const uint32_t SB = g.stage;
@@ -655,6 +754,12 @@ __global__ void __launch_bounds__(kG2Threads, 1)
     if (warp == 0) {
         // ------------------------------------------------------- producer
         if (lane == 0 && tb < te) {
+            uint64_t pol = 0;
+#if TG_G2_L2
+            // the split operands (17 MB at N = 65536, d = 64) are re-read by every CTA
+            // sweeping its tile rows; keep them in L2 against the 8.6 GB output stream
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
             Coord c = ltm_map(tb, kReciprocal, true);  // g(lambda) over the tile triangle
             uint64_t cur = ~0ull;
             uint32_t na = 0, q = 0, it = 0;
@@ -663,22 +768,17 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                     const uint32_t ns = it % kG2NormSlots, bar = BAR(NF + ns);
                     G2W(0, g2_wait_sleep(BAR(NE + ns), ((it / kG2NormSlots) & 1) ^ 1));
                     const uint32_t dst = smem_u32(sN + ns * kG2NormSlot);
-                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(136 * 4 + 128 * 4)
-                                 : "memory");
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                            dst),
-                        "l"(norms + c.j * kGT), "r"(136 * 4), "r"(bar)
-                        : "memory");
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                            dst + kG2NormRowOff),
-                        "l"(norms + c.i * kGT), "r"(128 * 4), "r"(bar)
-                        : "memory");
+                    g2_expect(bar, (wide ? 2 : 1) * (136 * 4 + 128 * 4));
+                    g2_copy(dst, norms + c.j * kGT, 136 * 4, bar, pol);
+                    g2_copy(dst + kG2NormRowOff, norms + c.i * kGT, 128 * 4, bar, pol);
+                    if (wide) {
+                        g2_copy(dst + kG2FacOff, facs + c.j * kGT, 136 * 4, bar, pol);
+                        g2_copy(dst + kG2FacOff + kG2NormRowOff, facs + c.i * kGT, 128 * 4, bar, pol);
+                    }
                 }
                 if (!as && c.i != cur) {
                     if (na > 0) G2W(1, g2_wait_sleep(BAR(1), (na - 1) & 1));  // MMAs done with the old row tile
-                    g2_bulk_load(smem_u32(sA), opA + c.i * nk * (uint64_t)kG2Slice, nk * kG2Slice, BAR(0));
+                    g2_bulk_load(smem_u32(sA), opA + c.i * nk * (uint64_t)kG2Slice, nk * kG2Slice, BAR(0), pol);
                     cur = c.i;
                     ++na;
                 }
@@ -687,24 +787,11 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                     G2W(2, g2_wait_sleep(BAR(BE + s), (round & 1) ^ 1));
                     const uint8_t* src = opB + k * 2 * g.bslice + c.j * 16 * (uint64_t)kG2Group;
                     const uint32_t dst = smem_u32(sB + s * SB) + boff, bar = BAR(BF + s);
-                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(SB)
-                                 : "memory");
+                    g2_expect(bar, SB);
                     if (as)  // the row tile's slice k rides along
-                        asm volatile(
-                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                                dst - kG2Slice),
-                            "l"(opA + (c.i * nk + k) * (uint64_t)kG2Slice), "r"(kG2Slice), "r"(bar)
-                            : "memory");
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                            dst),
-                        "l"(src), "r"(kG2BHalf), "r"(bar)
-                        : "memory");
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                            dst + kG2BHalf),
-                        "l"(src + g.bslice), "r"(kG2BHalf), "r"(bar)
-                        : "memory");
+                        g2_copy(dst - kG2Slice, opA + (c.i * nk + k) * (uint64_t)kG2Slice, kG2Slice, bar, pol);
+                    g2_copy(dst, src, kG2BHalf, bar, pol);
+                    g2_copy(dst + kG2BHalf, src + g.bslice, kG2BHalf, bar, pol);
                 }
             }
         }
@@ -753,8 +840,8 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         const uint32_t e = warp - 2, q = warp & 3, w4 = e >> 2;
         const uint32_t a = (q - (uint32_t)g.e_base) & 3u;  // (T(i) + j0 - e_base) mod 4, rows of quarter q
         const uint32_t s = (4u - a) & 3u;                    // first owned column of every row
-        const int sh = g2_scale_exp(__ldg(maxbits));
-        const float m2 = -2.0f * exp2f((float)(-2 * sh));
+        const int sh = g2_scale_exp(__ldg(bits));
+        const float m2g = -2.0f * exp2f((float)(-2 * sh));
         // quarter staging tile: row slot r (= TMEM lane 32q + r) x 33 chunks (32 used)
         float4* qbuf = reinterpret_cast<float4*>(sE + q * EPW * kG2EpiBytes);
         const uint32_t r_lane = g2_perm(32 * q + lane);  // compute phase: lane = TMEM lane
@@ -773,6 +860,8 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             G2W(6, g2_wait_sleep(BAR(NF + ns), (it / kG2NormSlots) & 1));
             const float ni = nslot[kG2NormRowOff / 4 + r_lane];
             const float4* nb4 = reinterpret_cast<const float4*>(nslot + WCOLS * w4);  // norms of loaded columns
+            const float4* cb4 = reinterpret_cast<const float4*>(nslot + kG2FacOff / 4 + WCOLS * w4);  // their 2^-s_j
+            const float m2 = wide ? -2.0f * nslot[(kG2FacOff + kG2NormRowOff) / 4 + r_lane] : m2g;
             G2W(7, g2_wait_sleep(BAR(AF + buf), (it / kG2Acc) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             const bool head = c.j == 0 && w4 == 0 && s > 0;  // warp-uniform: columns [0, s) of tile (i, 0)
@@ -794,18 +883,33 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             float dv[WCOLS];
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
-                switch (s) {
-                    case 0: g2_epi<0, 0>(v + 32 * h, nb4 + 8 * h, ni, m2, dv + 32 * h); break;
-                    case 1: g2_epi<1, 0>(v + 32 * h, nb4 + 8 * h, ni, m2, dv + 32 * h); break;
-                    case 2: g2_epi<2, 0>(v + 32 * h, nb4 + 8 * h, ni, m2, dv + 32 * h); break;
-                    default: g2_epi<3, 0>(v + 32 * h, nb4 + 8 * h, ni, m2, dv + 32 * h); break;
+                if (!wide) {
+                    switch (s) {
+                        case 0: g2_epi<0, 0>(v + 32 * h, nb4 + 8 * h, cb4, ni, m2, dv + 32 * h); break;
+                        case 1: g2_epi<1, 0>(v + 32 * h, nb4 + 8 * h, cb4, ni, m2, dv + 32 * h); break;
+                        case 2: g2_epi<2, 0>(v + 32 * h, nb4 + 8 * h, cb4, ni, m2, dv + 32 * h); break;
+                        default: g2_epi<3, 0>(v + 32 * h, nb4 + 8 * h, cb4, ni, m2, dv + 32 * h); break;
+                    }
+                } else {
+                    switch (s) {
+                        case 0: g2_epi<0, 0, true>(v + 32 * h, nb4 + 8 * h, cb4 + 8 * h, ni, m2, dv + 32 * h); break;
+                        case 1: g2_epi<1, 0, true>(v + 32 * h, nb4 + 8 * h, cb4 + 8 * h, ni, m2, dv + 32 * h); break;
+                        case 2: g2_epi<2, 0, true>(v + 32 * h, nb4 + 8 * h, cb4 + 8 * h, ni, m2, dv + 32 * h); break;
+                        default: g2_epi<3, 0, true>(v + 32 * h, nb4 + 8 * h, cb4 + 8 * h, ni, m2, dv + 32 * h); break;
+                    }
                 }
             }
             float nh0 = 0.0f, nh1 = 0.0f, nh2 = 0.0f;  // column norms 0..2 (head cells)
+            float ch[3] = {1.0f, 1.0f, 1.0f};         // and their factors (wide range)
             if (head) {
                 nh0 = nslot[0];
                 nh1 = nslot[1];
                 nh2 = nslot[2];
+                if (wide) {
+                    ch[0] = nslot[kG2FacOff / 4];
+                    ch[1] = nslot[kG2FacOff / 4 + 1];
+                    ch[2] = nslot[kG2FacOff / 4 + 2];
+                }
             }
             __syncwarp();
             if (lane == 0) g2_arrive(BAR(NE + ns));  // norm slot consumed
@@ -819,7 +923,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                 const float nhv[3] = {nh0, nh1, nh2};
 #pragma unroll
                 for (uint32_t p = 0; p < 3; ++p)
-                    if (p < s && p <= i) rowp[p] = (p == i) ? 0.0f : g2_dist(v[WCOLS + p], ni, nhv[p], m2);
+                    if (p < s && p <= i) rowp[p] = (p == i) ? 0.0f : g2_dist(v[WCOLS + p], ni, nhv[p], m2, ch[p]);
             }
             g2_bar_quarter(q);  // the quarter's previous tile is fully read
 #pragma unroll

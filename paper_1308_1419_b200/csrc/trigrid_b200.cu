@@ -736,17 +736,20 @@ tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, ui
     const uint64_t bslice = (nt * 16 + 1) * (uint64_t)kG2Group;
     const uint64_t b_bytes = nk * 2 * bslice;
     Scratch sn, so;
-    TG_TRY(scratch_alloc(sn, (n_pad + 8) * sizeof(float), st));
+    // norms | per-point scale factors | per-point max |x| bits, (n_pad + 8) each
+    TG_TRY(scratch_alloc(sn, 3 * (n_pad + 8) * sizeof(float), st));
     TG_TRY(scratch_alloc(so, a_bytes + b_bytes + 256, st));
     float* norms = static_cast<float*>(sn.p);
+    float* facs = norms + (n_pad + 8);
+    unsigned int* pmax = reinterpret_cast<unsigned int*>(facs + (n_pad + 8));
     uint8_t* opA = static_cast<uint8_t*>(so.p);
     uint8_t* opB = opA + a_bytes;
-    unsigned int* maxbits = reinterpret_cast<unsigned int*>(opB + b_bytes);
-    TG_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(unsigned int), st));
+    unsigned int* bits = reinterpret_cast<unsigned int*>(opB + b_bytes);  // max |x|, ~min nonzero point max
+    TG_CUDA(cudaMemsetAsync(bits, 0, 2 * sizeof(unsigned int), st));
     const unsigned pb = (unsigned)std::min<uint64_t>(ceil_div(n_pad + 8, 256), (uint64_t)c->sms * 8);
-    gram_prep_kernel<<<pb, 256, 0, st>>>(pts, n, n_pad + 8, d, norms, maxbits);
+    gram_prep_kernel<<<pb, 256, 0, st>>>(pts, n, n_pad + 8, d, norms, pmax, bits);
     const unsigned sb = (unsigned)std::min<uint64_t>(ceil_div((n_pad + 8) * nk * 8, 256), (uint64_t)c->sms * 16);
-    gram_split_kernel<<<sb, 256, 0, st>>>(pts, n, n_pad, d, nk, maxbits, opA, opB, bslice);
+    gram_split_kernel<<<sb, 256, 0, st>>>(pts, n, n_pad, d, nk, bits, pmax, facs, opA, opB, bslice);
     Gram2Geom g{};
     g.n = n;
     g.nk = nk;
@@ -767,7 +770,7 @@ tg_status launch_gram2_edm(uint64_t n, uint32_t d, uint32_t rho, uint64_t b0, ui
     const uint64_t grid = std::min<uint64_t>(tiles, (uint64_t)c->sms);
     g.per_cta = ceil_div(tiles, grid);
     gram2_edm_kernel<<<(unsigned)ceil_div(tiles, g.per_cta), kG2Threads, g2_smem_bytes(nk, g.ring, g.a_stream != 0), st>>>(
-        g, opA, opB, norms, maxbits, out);
+        g, opA, opB, norms, facs, bits, out);
     g_launches += 3;
     TG_CUDA(cudaGetLastError());
     return TG_OK;

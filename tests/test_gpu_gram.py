@@ -77,6 +77,24 @@ def test_gram_tolerance_adversarial(tg, orc, cuda, kind):
     _check(orc, pts, _gram(tg, cuda, pts))
 
 
+@pytest.mark.parametrize("ratio,d", [(1e-5, 64), (1e-8, 64), (1e-11, 64), (1e-8, 200), (1e-9, 3), (1e-20, 64)])
+def test_gram_tolerance_wide_range(tg, orc, cuda, ratio, d):
+    """Per-point magnitudes spread over more than 2^20: with one
+    global fp16 scale the small points fall to fp16's subnormal floor; the
+    kernel switches to per-point scales and the stated bound holds for every
+    pair -- small vs small (incl. exact duplicates and all-zero points), small
+    vs large, large vs large."""
+    n = 600
+    pts = orc.gen_points(n, d, 5).astype(np.float64) - 0.5
+    small = np.arange(n) % 3 != 0
+    pts[~small] *= 1e3
+    pts[small] *= 1e3 * ratio
+    pts[4::9] = pts[1::9][: pts[4::9].shape[0]]  # duplicates among the small points
+    pts[7] = 0.0
+    pts = pts.astype(np.float32)
+    _check(orc, pts, _gram(tg, cuda, pts))
+
+
 def test_gram_concurrent_streams(tg, orc, cuda):
     """Two host threads, two streams, different inputs: the per-launch device
     scratch (operands, norms) is private, so each result equals its serial run."""
