@@ -13,6 +13,7 @@
 #include <string>
 #include <thread>
 #include <vector>
+#include <numeric>
 
 #include "../../include/trigrid_b200.h"
 #include "tg_gram.cuh"
@@ -443,29 +444,74 @@ uint64_t utm_runs() {
 
 tg_status plan_span_c(const Problem& P, const Window& w, uint32_t C, SpanGeom* g, int only_pass);
 
-// Units a launch should have at least: ~32 warps' worth per SM.  A small
+// LTM span units: row-aligned lambda segments (default) or, A/B
+// TG_LTM_ROWS=0, runs of C consecutive lambda that may cross row ends.
+bool ltm_row_units() {
+    static bool v = [] {
+        const char* e = std::getenv("TG_LTM_ROWS");
+        return !e || std::atoi(e) != 0;
+    }();
+    return v;
+}
+
+// Live units a launch should have at least: ~16 warps' worth per SM.  A small
 // problem planned with the default C (16 blocks per warp) leaves most SMs idle
 // and each warp on a long serial run walk (N=1024 LTM: 133 warps, 56 us vs
-// 15 us for BB), so C shrinks until the launch has this many units.
+// 15 us for BB), so C shrinks until the launch has this many units that do
+// work.  Counted on LIVE blocks (BB's discarded x > y blocks excluded): with
+// the grid count BB kept twice LTM's run length at the same N and LTM's
+// 16-column runs at N=2048 left 7/8 of the lanes idle (CUDA-graph replay:
+// LTM write 18.5 us vs BB 12.7 us at N=2048, 20.5 vs 13.7 us at N=4096).
 uint64_t min_span_units() {  // A/B: TG_SPAN_MIN_UNITS
     static uint64_t v = [] {
         const char* e = std::getenv("TG_SPAN_MIN_UNITS");
-        return e ? (uint64_t)std::atoll(e) : (uint64_t)148 * 32;
+        return e ? (uint64_t)std::atoll(e) : (uint64_t)148 * 16;
     }();
     return v;
+}
+
+// Grid blocks of the launch that emit tiles (BB: the y >= x half; LTM: the
+// lambda range without the balanced-grid padding; the pass-table and UTM
+// plans have no discarded units).
+uint64_t live_span_blocks(const SpanGeom& g) {
+    if (g.strat == kSpanBB) return tri(g.W) - tri(g.b0);
+    if (g.strat == kSpanLTM) return g.lam1 - g.lam0;
+    return g.units * g.C;
 }
 
 // Geometry for the window's block rows; `adaptive` lets C shrink for small
 // problems (the one-CTA-per-run d > 4 kernel needs the fixed C).  only_pass
 // (REC, >= 0): plan that grid pass alone (LaunchOptions::per_pass timing).
+// A/B: TG_SPAN_PERM=f (f in (0, 1), e.g. 0.618) runs the units in the order
+// u -> (u * p) % units, p ~ f * units coprime to units; 0 / unset = identity.
+double span_perm_frac() {
+    static double v = [] {
+        const char* e = std::getenv("TG_SPAN_PERM");
+        return e ? std::atof(e) : 0.0;
+    }();
+    return v;
+}
+
+void set_span_perm(SpanGeom* g) {
+    g->perm = 0;
+    const double f = span_perm_frac();
+    if (f <= 0.0 || f >= 1.0 || g->units < 3 || g->units > 0xffffffffull) return;
+    uint64_t p = std::max<uint64_t>(1, (uint64_t)(f * (double)g->units));
+    while (std::gcd(p, g->units) != 1) ++p;
+    g->perm = p;
+}
+
 tg_status plan_span(const Problem& P, const Window& w, uint32_t C, SpanGeom* g, bool adaptive = true,
                     int only_pass = -1) {
     TG_TRY(plan_span_c(P, w, C, g, only_pass));
     const uint64_t min_units = min_span_units();
-    if (!adaptive || C <= 1 || g->units >= min_units) return TG_OK;
-    const uint64_t blocks = g->units * C;  // upper bound of the launch's grid blocks
-    const uint32_t c2 = (uint32_t)std::max<uint64_t>(1, blocks / min_units);
-    return c2 < C ? plan_span_c(P, w, c2, g, only_pass) : TG_OK;
+    const uint64_t live = live_span_blocks(*g);
+    if (adaptive && C > 1 && ceil_div(live, C) < min_units) {
+        const uint32_t c2 = (uint32_t)std::max<uint64_t>(1, live / min_units);
+        if (c2 < C) TG_TRY(plan_span_c(P, w, c2, g, only_pass));
+    }
+    set_span_perm(g);
+    return TG_OK;
 }
 
 void add_pass(SpanGeom* g, uint64_t& unit, uint64_t y0, uint64_t y1, uint64_t sb, uint64_t side, uint32_t level,
@@ -506,6 +552,16 @@ tg_status plan_span_c(const Problem& P, const Window& w, uint32_t C, SpanGeom* g
         const uint64_t side = L ? ceil_sqrt(L) : 0;
         g->vb_count = side * side;  // balanced grid (tri.cpp:23-26) incl. padding
         g->units = ceil_div(g->vb_count, C);
+        g->b1 = b1;
+        if (ltm_row_units()) {  // row-aligned lambda segments: U(r) units before block row r
+            auto U = [C](uint64_t r) {
+                const uint64_t q = r / C, t = r % C;
+                return C * (q * (q + 1) / 2) + t * (q + 1);
+            };
+            g->ltm_rows = 1;
+            g->ubase = U(b0);
+            g->units = U(b1) - U(b0);
+        }
     } else if (s == TG_REC) {
         g->strat = kSpanREC;
         g->m = P.m;
@@ -968,6 +1024,15 @@ bool collide_v1() {
     return v;
 }
 
+// A/B switch: TG_COLLIDE_V2=1 keeps the second span collision kernel (unpaired operands, select trees).
+bool collide_v2() {
+    static bool v = [] {
+        const char* e = std::getenv("TG_COLLIDE_V2");
+        return e && std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 // The td-kernel launch behind tg_launch (launch_dummy / launch_edm /
 // launch_count / launch, engine.cpp:150-203) for a validated problem.  Per-pass
 // device times go to o.per_pass (LaunchOptions::per_pass, engine.cpp:87-133):
@@ -1348,10 +1413,24 @@ tg_status tg_collide(tg_strategy s, uint64_t n, uint32_t rho, const float* spher
             // partial words at row-segment ends are OR-ed into a zeroed table
             TG_CUDA(cudaMemsetAsync(bits, 0, ceil_div(p1 - p0, 32) * 4, st));
             const uint64_t grid2 = span_grid(g, o.persistent != 0, c->sms, 32, kCollideWarps);
-            span_collide2_kernel<TG_COLLIDE_SLOTS><<<(unsigned)grid2, kCollideWarps * 32, 0, st>>>(
-                g, p0, reinterpret_cast<const float4*>(spheres), r_max, bits,
-                reinterpret_cast<unsigned long long*>(hits));
-            ++g_launches;
+            const float4* sph4 = reinterpret_cast<const float4*>(spheres);
+            unsigned long long* h = reinterpret_cast<unsigned long long*>(hits);
+            if (collide_v2()) {
+                span_collide2_kernel<TG_COLLIDE_SLOTS><<<(unsigned)grid2, kCollideWarps * 32, 0, st>>>(
+                    g, p0, sph4, r_max, bits, h);
+                ++g_launches;
+            } else {
+                // pre-paired column operands (qa, qb: 2 x 16 B per sphere), private to the launch
+                Scratch sq;
+                TG_TRY(scratch_alloc(sq, (size_t)n * 2 * sizeof(float4), st));
+                float4* qa = static_cast<float4*>(sq.p);
+                float4* qb = qa + n;
+                collide_pairs_prep_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(n, 256), (uint64_t)c->sms * 8), 256, 0,
+                                            st>>>(sph4, n, r_max, qa, qb);
+                span_collide3_kernel<TG_COLLIDE_SLOTS><<<(unsigned)grid2, kCollideWarps * 32, 0, st>>>(
+                    g, p0, sph4, qa, qb, r_max, bits, h);
+                g_launches += 2;
+            }
             TG_CUDA(cudaGetLastError());
         }
     } else {
