@@ -386,18 +386,47 @@ def run_ours(args):
     other = {}
     if not args.quick and world == 1:
         # C2: write / dummy td-kernel sweep over N, every mapping (I = t_BB / t_strategy)
+        # Each entry is the device time per launch of a CUDA graph of k
+        # back-to-back launches (no host launch gaps: at N <= 4096 a launch is
+        # ~10 us, below the Python + ctypes launch cost).
+        def graph_ms(fn, k):
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                for _ in range(2):
+                    fn(side)
+            torch.cuda.synchronize(dev)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=side):
+                for _ in range(k):
+                    fn(side)
+            ts = []
+            with torch.cuda.stream(side):
+                gr.replay()
+                for _ in range(3):
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record(side)
+                    gr.replay()
+                    b.record(side)
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b) / k)
+            del gr
+            return sorted(ts)[1]
+
         sweep = {}
-        for ns in (1024, 4096, 16384, 65536):
+        for ns in (1024, 2048, 4096, 8192, 16384, 65536):
             wb = torch.empty(tri(ns), dtype=torch.int32, device=dev)
             row = {}
-            for mode, strats in (("grid", ("bb", "ltm-r", "utm", "rb", "rec")), ("span", ("bb", "ltm-r", "rec"))):
+            for mode, strats in (("grid", ("bb", "ltm-r", "utm", "rb", "rec")),
+                                 ("span", ("bb", "ltm-r", "utm", "rb", "rec"))):
                 for s in strats:
-                    k = 3 if (ns == 65536 and mode == "grid") else 10
-                    w_ms = time_steps(lambda: tg.launch("write", s, ns, out=wb, rho=RHO, mode=mode, stream=stream,
-                                                        sync=False), k, 2)
+                    k = 2 if (ns == 65536 and mode == "grid") else (5 if ns == 65536 else 20)
+                    w_ms = graph_ms(lambda st_: tg.launch("write", s, ns, out=wb, rho=RHO, mode=mode, stream=st_,
+                                                          sync=False), k)
                     r = {"write_ms": w_ms, "write_gbs": 4 * tri(ns) / (w_ms / 1e3) / 1e9}
-                    r["dummy_ms"] = time_steps(lambda: tg.launch("dummy", s, ns, rho=RHO, mode=mode, stream=stream,
-                                                                 sync=False), k, 2)
+                    r["dummy_ms"] = graph_ms(lambda st_: tg.launch("dummy", s, ns, rho=RHO, mode=mode, stream=st_,
+                                                                   sync=False), k)
                     row[f"{mode}/{s}"] = r
             for key, r in row.items():
                 bbr = row[key.split("/")[0] + "/bb"]
@@ -407,6 +436,8 @@ def run_ours(args):
             sweep[str(ns)] = row
             del wb
         other["C2_write_dummy_sweep"] = sweep
+        other["C2_timing"] = ("device ms per launch: median of 3 replays of a CUDA graph of k back-to-back launches "
+                              "(k = 20; 5 at N=65536 span, 2 grid); I = t_BB / t_strategy in the same mode")
     if not args.quick:
         # C3: collision table N=32768 (bit-packed no-diagonal table + count)
         nc, r_max = 32768, 0.0625
