@@ -138,6 +138,22 @@ def golden_sha(n: int, d: int, rank: int, world: int):
     return sh["sha256"][rank] if sh else None
 
 
+def golden_collide(n: int, r_max: float, rank: int, world: int):
+    """(sha256, hits) of this rank's collision bit table (tests/golden/
+    golden_large.json, from the oracle), or None."""
+    p = os.path.join(ROOT, "tests", "golden", "golden_large.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        ref = json.load(f).get("collide", {}).get(f"{n}|{r_max}")
+    if not ref:
+        return None
+    if world == 1:
+        return ref["sha256"], ref["hits"]
+    sh = ref.get("shards", {}).get(str(world))
+    return (sh["sha256"][rank], sh["hits"][rank]) if sh else None
+
+
 def sha256_device(t, chunk_bytes: int = 1 << 28) -> str:
     """sha256 of a CUDA tensor's bytes through a pinned staging buffer
     (outside every timed region)."""
@@ -235,7 +251,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1308_1419_b200 import _lib
+    from paper_1308_1419_b200 import _lib, multi
     from paper_1308_1419_b200 import trigrid as tg
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -258,11 +274,7 @@ def run_ours(args):
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=cdev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return multi.max_over_ranks(x, device=cdev)
 
     n, d, strategy = args.n, args.d, args.strategy
     shard = (rank, world) if world > 1 else None
@@ -444,10 +456,20 @@ def run_ours(args):
         sph = tg.gen_values(nc * 4, SEED, dev).view(nc, 4)
         c_ms = time_steps(lambda: tg.collide(sph, r_max, strategy="ltm-r", shard=(rank, world) if world > 1 else None,
                                              stream=stream, sync=False), 5, 2)
-        _, hits = tg.collide(sph, r_max, strategy="ltm-r", shard=(rank, world) if world > 1 else None)
+        bits, hits = tg.collide(sph, r_max, strategy="ltm-r", shard=(rank, world) if world > 1 else None)
         p0, p1 = tg.shard_elems(nc, RHO, rank, world, with_diag=False)
+        hits_shard = int(hits.item())
+        c3_ref = golden_collide(nc, r_max, rank, world)
+        c3_sha = sha256_device(bits)
+        del bits
         other["C3_collide_n32768"] = {"ms": c_ms, "pairs_per_s": tri(nc - 1) / (c_ms / 1e3),
-                                      "hits_shard": int(hits.item()), "r_max": r_max,
+                                      "hits_shard": hits_shard,
+                                      "hits_total": multi.reduce_hits(hits.to(cdev) if world > 1 else hits),
+                                      "r_max": r_max,
+                                      "verify": {"ok": bool(c3_ref) and c3_sha == c3_ref[0] and hits_shard == c3_ref[1],
+                                                 "sha256": c3_sha, "want_sha256": c3_ref[0] if c3_ref else None,
+                                                 "want_hits": c3_ref[1] if c3_ref else None,
+                                                 "golden": "tests/golden/golden_large.json collide (oracle)"},
                                       "out_bytes_shard": 4 * ((p1 - p0 + 31) // 32)}
         # C4: EDM N=65536, d=64, direct (bit-exact) wide span kernel
         if True:

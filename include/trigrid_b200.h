@@ -154,6 +154,9 @@ int tg_rb_map(uint64_t tx, uint64_t ty, uint64_t n, uint64_t* i, uint64_t* j);
 int tg_rec_decompose(uint64_t n, uint32_t rho, uint64_t* m, uint32_t* k);
 /* count_wasted (engine.cpp:205-217): bb and ltm-* only, else TG_EINVAL. */
 tg_status tg_count_wasted(tg_strategy s, uint64_t n, uint64_t* out);
+/* ltm_diag_waste_blocks (engine.hpp:87, engine.cpp:219-221): n / 2, the LTM
+ * diagonal blocks' half-empty share counted in blocks. */
+double tg_ltm_diag_waste_blocks(uint64_t n);
 /* improvement_model (bench.cpp:138-144). */
 tg_status tg_improvement_model(double beta, double tau, double n, double* out);
 /* Strategy name <-> id (parse_strategy strategies.cpp:19-28 + "ltm-exact"). */

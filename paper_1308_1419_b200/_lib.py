@@ -74,6 +74,7 @@ _SIGS = {
     "tg_rb_map": (C.c_int, [_u64, _u64, _u64, _pu64, _pu64]),
     "tg_rec_decompose": (C.c_int, [_u64, _u32, _pu64, C.POINTER(C.c_uint32)]),
     "tg_count_wasted": (_st, [C.c_int, _u64, _pu64]),
+    "tg_ltm_diag_waste_blocks": (C.c_double, [_u64]),
     "tg_improvement_model": (_st, [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]),
     "tg_parse_strategy": (_st, [C.c_char_p, C.POINTER(C.c_int)]),
     "tg_dispatch_stats_for": (_st, [C.c_int, _u64, _u32, _u32, _u32, _pstats]),

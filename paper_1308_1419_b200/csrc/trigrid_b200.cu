@@ -1319,6 +1319,8 @@ tg_status tg_count_wasted(tg_strategy s, uint64_t n, uint64_t* out) {
     return fail(TG_EINVAL, "count_wasted: no closed form for this strategy");
 }
 
+double tg_ltm_diag_waste_blocks(uint64_t n) { return static_cast<double>(n) / 2.0; }
+
 tg_status tg_improvement_model(double beta, double tau, double n, double* out) {
     if (!(beta > 0.0) || !(tau > 0.0))
         return fail(TG_EINVAL, "improvement_model: beta and tau must be positive");

@@ -57,15 +57,3 @@ def reduce_hits(hits, device=None) -> int:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return int(t.item())
-
-
-def edm_shard(points, rank: int, world: int, strategy: str = "ltm-r", rho: int = 16, **kw):
-    """This rank's packed EDM slice (device tensor) of the whole problem."""
-    return tg.edm(points, strategy=strategy, rho=rho, shard=(rank, world) if world > 1 else None, **kw)
-
-
-def collide_all(spheres, r_max: float, rank: int, world: int, strategy: str = "ltm-r", rho: int = 16, **kw):
-    """This rank's collision bit slice plus the global hit count (all-reduced)."""
-    bits, hits = tg.collide(spheres, r_max, strategy=strategy, rho=rho,
-                            shard=(rank, world) if world > 1 else None, **kw)
-    return bits, reduce_hits(hits, spheres.device)

@@ -193,6 +193,11 @@ def count_wasted(strategy: str, n) -> int:
     return out.value
 
 
+def ltm_diag_waste_blocks(n) -> float:
+    """engine.cpp:219-221: n / 2 (no pybind binding in the reference; C++ surface)."""
+    return float(_L().tg_ltm_diag_waste_blocks(_u64(n, "n")))
+
+
 def improvement_model(beta: float, tau: float, n: float) -> float:
     """Modeled improvement factor 2*beta*n^2/(tau*n^2 + tau*n) (bench.cpp:138-144)."""
     out = C.c_double()

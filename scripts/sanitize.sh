@@ -19,10 +19,14 @@ for tool in memcheck racecheck; do
   run write_ltm $tool write --n 3000 --strategy ltm-r --mode span
   run write_utm $tool write --n 3000 --strategy utm --mode span
   run collide $tool collide --n 3000 --strategy ltm-r
+  run collide_bb $tool collide --n 2047 --strategy bb
+  run write_rb $tool write --n 2999 --strategy rb --mode span
+  run write_bb $tool write --n 3001 --strategy bb --mode span
   run edm_d64_direct $tool edm --n 1500 --d 64 --strategy ltm-r --mode span
   run edm_d64_gram $tool edm --n 1500 --d 64 --strategy ltm-r --mode gram
   run edm_d200_gram $tool edm --n 700 --d 200 --strategy ltm-r --mode gram
 done
 run edm_d64_gram synccheck edm --n 1500 --d 64 --strategy ltm-r --mode gram
 run edm_d64_direct synccheck edm --n 1500 --d 64 --strategy ltm-r --mode span
+run collide synccheck collide --n 3000 --strategy ltm-r
 cat gpurun_out/sanitize_summary.txt

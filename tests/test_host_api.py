@@ -87,6 +87,9 @@ def test_scalars_golden(tg, golden):
         assert tg.sqrt_via(e, x) == w
     for s, n, w in golden["count_wasted"]:
         assert tg.count_wasted(s, n) == w
+    # ltm_diag_waste_blocks (engine.cpp:219-221): n / 2 as a double
+    for n in (1, 2, 3, 1920, 4097, 1 << 20):
+        assert tg.ltm_diag_waste_blocks(n) == n / 2.0
     for b, t, n, w in golden["improvement_model"]:
         assert tg.improvement_model(b, t, n) == w
     assert tg.tri_count(4) == 10 and tg.tri_count(1920) == 1844160 and tg.tri_count(5, False) == 10
