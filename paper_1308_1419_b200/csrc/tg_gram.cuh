@@ -671,8 +671,11 @@ __device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, con
                 d0 = r.x;
                 d1 = r.y;
             } else {
-                asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(fmaxf(d2.x, 0.0f)));
-                asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(fmaxf(d2.y, 0.0f)));
+                // sqrt(|d^2|): a rounding-negative d^2 (true value >= 0) gives
+                // ||c| - e| <= |c - e|, so the stated d^2 tolerance still holds and the
+                // clamp folds into MUFU's |x| operand modifier (no FMNMX per cell)
+                asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(fabsf(d2.x)));
+                asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(fabsf(d2.y)));
             }
             dv[p] = d0;
             dv[p + 1] = d1;
