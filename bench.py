@@ -341,7 +341,7 @@ def run_ours(args):
             traffic = json.load(f).get(f"edm_{strategy}_n{n}_d{d}_g{world}")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-                "kernel": "tg::span_edm_kernel<3,1> (+ classify_points_kernel)",
+                "kernel": "tg::span_edm_kernel<3,2,1> (+ classify_points_kernel)",
                 "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": k_ms,
                 "launch_ms_median_isolated": k_med,
                 "timing": "CUDA events over the timed region (launch_ms = its average per step); "
