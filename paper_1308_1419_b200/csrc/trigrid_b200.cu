@@ -723,7 +723,7 @@ tg_status launch_wide2_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float
 // d > 4: CTA-per-run tiled kernel (rho == 16, runs of <= 128 columns).
 tg_status launch_wide_edm(uint32_t d, const SpanGeom& g, OutWin ow, const float* pts, float* out,
                           const unsigned int* flag, cudaStream_t st, bool persistent, int sms, DeviceCtx* c) {
-    if (g.rho != 16 || g.C != 8) return fail(TG_EINVAL, "wide EDM span kernel needs rho == 16");
+    if (g.rho != 16 || g.C != (wide_v1() ? 8u : 8u * kW2CH)) return fail(TG_EINVAL, "wide EDM span kernel needs rho == 16");
     if (!wide_v1()) return launch_wide2_edm(d, g, ow, pts, out, flag, st, persistent, sms, c);
     uint64_t grid = std::min<uint64_t>(g.units, 0x7fffffffull);
     if (persistent) {
@@ -1124,7 +1124,8 @@ tg_status launch_impl(tg_kernel kernel, const Problem& P, uint32_t d, const floa
     Timer timer(st, !o.async);
     if (span) {
         const bool wide = kernel == TG_KERNEL_EDM && d > 4;
-        const int slots = wide ? 1 : ((kernel == TG_KERNEL_WRITE || kernel == TG_KERNEL_COUNT) ? write_slots()
+        const int slots = wide ? (wide_v1() ? 1 : kW2CH)
+                               : ((kernel == TG_KERNEL_WRITE || kernel == TG_KERNEL_COUNT) ? write_slots()
                                                                                               : span_slots());
         const uint32_t C = std::max<uint32_t>(1, (uint32_t)(128 * slots) / rho);
         Scratch fs;
