@@ -439,6 +439,13 @@ def run_ours(args):
                     r = {"write_ms": w_ms, "write_gbs": 4 * tri(ns) / (w_ms / 1e3) / 1e9}
                     r["dummy_ms"] = graph_ms(lambda st_: tg.launch("dummy", s, ns, rho=RHO, mode=mode, stream=st_,
                                                                    sync=False), k)
+                    # cells/s of the write and dummy kernels, grid blocks/s and
+                    # the wasted-block fraction of the strategy's grid (closed form, reference tallies)
+                    ds = tg.dispatch_stats(s, ns, RHO)
+                    r["write_cells_per_s"] = tri(ns) / (w_ms / 1e3)
+                    r["dummy_cells_per_s"] = tri(ns) / (r["dummy_ms"] / 1e3)
+                    r["grid_blocks_per_s"] = ds["blocks_launched"] / (r["dummy_ms"] / 1e3)
+                    r["wasted_block_frac"] = ds["blocks_discarded"] / max(1, ds["blocks_launched"])
                     row[f"{mode}/{s}"] = r
             for key, r in row.items():
                 bbr = row[key.split("/")[0] + "/bb"]
