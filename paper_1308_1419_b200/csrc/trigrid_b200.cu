@@ -433,13 +433,21 @@ bool span_eligible(tg_strategy s, uint32_t rho) {
 // multiples: the d > 4 kernels, the collision kernel).
 bool square_tiles(tg_strategy s) { return s == TG_BB || is_ltm(s) || s == TG_REC; }
 
-// UTM super-block side in run widths.  A/B: TG_UTM_RUNS.
-uint64_t utm_runs() {
-    static uint64_t v = [] {
+// UTM super-block side in run widths: about 4 super-block rows per launch,
+// within [16, 64].  utm_pair orders the super-blocks column by column, so the
+// 32-byte sectors split across a vertical super-block boundary are completed
+// long after their first half was written: evicted half-written sectors cost
+// a DRAM read-modify-write (ncu: the UTM write kernel reads 20.8 MB vs 2.4 MB
+// for LTM).  Fewer, wider super-blocks at large N: A/B at N=65536 (runs 16 /
+// 32 / 64 / 128): write 1.488 / 1.425 / 1.370 / 1.347 ms, EDM 1.607 / 1.59 /
+// 1.578 / 1.621 ms.  A/B: TG_UTM_RUNS.
+uint64_t utm_runs(uint64_t n, uint64_t run_cols) {
+    static int env = [] {
         const char* e = std::getenv("TG_UTM_RUNS");
-        return e ? (uint64_t)std::max(1, std::atoi(e)) : 16ull;
+        return e ? std::max(1, std::atoi(e)) : 0;
     }();
-    return v;
+    if (env) return (uint64_t)env;
+    return std::min<uint64_t>(64, std::max<uint64_t>(16, ceil_div(n, 4 * run_cols)));
 }
 
 tg_status plan_span_c(const Problem& P, const Window& w, uint32_t C, SpanGeom* g, int only_pass);
@@ -601,7 +609,7 @@ tg_status plan_span_c(const Problem& P, const Window& w, uint32_t C, SpanGeom* g
         g->engine = P.engine;
         // super-blocks of W = utm_runs() run widths (C rho columns each); one
         // unit per 16-row x run tile
-        const uint64_t runs = utm_runs(), S = (uint64_t)C * rho * runs, R0 = std::min(n, b0 * rho);
+        const uint64_t runs = utm_runs(n, (uint64_t)C * rho), S = (uint64_t)C * rho * runs, R0 = std::min(n, b0 * rho);
         const uint64_t He = w.r_hi - R0;
         g->W = S;
         g->ur = runs;
