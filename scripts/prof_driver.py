@@ -14,7 +14,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("kernel", choices=["edm", "write", "collide"])
+    ap.add_argument("kernel", choices=["edm", "write", "collide", "dummy"])
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--d", type=int, default=3)
     ap.add_argument("--strategy", default="ltm-r")
@@ -41,6 +41,18 @@ def main():
             ms = ts[len(ts) // 2]
             print(f"collide n={n} {a.strategy} mode={a.mode}: median {ms:.4f} ms "
                   f"({n * (n - 1) / 2 / ms / 1e9:.1f} G pairs/s) over {a.reps}")
+    elif a.kernel == "dummy":
+        ts = []
+        for _ in range(a.reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            tg.launch("dummy", a.strategy, n, mode=a.mode)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        if a.time:
+            ts.sort()
+            print(f"dummy n={n} {a.strategy} mode={a.mode}: median {ts[len(ts) // 2]:.4f} ms over {a.reps}")
     else:
         out = torch.empty(n * (n + 1) // 2, dtype=torch.float32 if a.kernel == "edm" else torch.int32, device="cuda")
         pts = tg.gen_values(n * a.d, 42).view(n, a.d) if a.kernel == "edm" else None
