@@ -17,6 +17,15 @@ def _rec_ok(orc, n, rho):
     return orc.rec_decompose(n, rho) is not None
 
 
+def test_utm_superblock_widths(tg, cuda):
+    """The UTM super-block side scales with N (16..64 run widths, about 4
+    super-block rows): exactly-once coverage around the sizes where it
+    changes (16 -> 32 -> 64) and at odd N (ragged last super-block)."""
+    for n in (16383, 16385, 20000, 32768, 40000, 65535):
+        r = tg.coverage("utm", n, 16, mode="span")
+        assert r["ok"], (n, r)
+
+
 @pytest.mark.parametrize("strat", SPAN7)
 def test_span_coverage_exactly_once(tg, orc, cuda, strat):
     """COUNT in span form adds 1 to every cell of every owned chunk: each cell
