@@ -476,7 +476,8 @@ def run_ours(args):
                                       "verify": {"ok": bool(c3_ref) and c3_sha == c3_ref[0] and hits_shard == c3_ref[1],
                                                  "sha256": c3_sha, "want_sha256": c3_ref[0] if c3_ref else None,
                                                  "want_hits": c3_ref[1] if c3_ref else None,
-                                                 "golden": "tests/golden/golden_large.json collide (oracle)"},
+                                                 "golden": "tests/golden/golden_large.json collide (oracle)"
+                                                 + ("" if c3_ref else f" -- no entry for {world} shards")},
                                       "out_bytes_shard": 4 * ((p1 - p0 + 31) // 32)}
         # C4: EDM N=65536, d=64, direct (bit-exact) wide span kernel
         if True:
