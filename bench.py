@@ -444,8 +444,8 @@ def run_ours(args):
         for ns in (1024, 2048, 4096, 8192, 16384, 65536):
             wb = torch.empty(tri(ns), dtype=torch.int32, device=dev)
             row = {}
-            for mode, strats in (("grid", ("bb", "ltm-r", "utm", "rb", "rec")),
-                                 ("span", ("bb", "ltm-r", "utm", "rb", "rec"))):
+            c2_strats = ("bb", "ltm-r", "ltm-x", "ltm-n", "utm", "rb", "rec")
+            for mode, strats in (("grid", c2_strats), ("span", c2_strats)):
                 for s in strats:
                     k = 2 if (ns == 65536 and mode == "grid") else (5 if ns == 65536 else 20)
                     w_ms = graph_ms(lambda st_: tg.launch("write", s, ns, out=wb, rho=RHO, mode=mode, stream=st_,
