@@ -306,8 +306,9 @@ __global__ void gram_norms_kernel(const float* __restrict__ pts, uint64_t n, uin
 //  * Roles: warp 0 = bulk-copy producer (row tile resident while the tile row
 //    stays, column operands through a ring of stages), warp 1 = MMA issuer (per
 //    64-feature slice 3 x 4 tcgen05.mma M=128 N=136 K=16: hi*lo + lo*hi +
-//    hi*hi), warps 2..17 = epilogue: TMEM lane quarter warp % 4 (32 rows) x 8
-//    of the 32 chunks.  kG2Acc accumulators in TMEM let the MMAs run ahead.
+//    hi*hi), warps 2..17 = epilogue: TMEM lane quarter warp % 4, split into two
+//    2-warp sync groups of 16 rows (TG_G2_SUB; tcgen05.ld 16x32bx2, each warp
+//    64 of the 128 columns).  kG2Acc accumulators in TMEM let the MMAs run ahead.
 //  * Epilogue per warp: tcgen05.ld (32 rows x 40 columns) -> release the
 //    accumulator -> d = sqrt(max(|x_i|^2 + |x_j|^2 - 2 g, 0)) on the 32 owned
 //    columns (warp-uniform compile-time selection of the shift) -> 8 chunks
@@ -686,9 +687,48 @@ __device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, con
     }
 }
 
+#ifndef TG_G2_SUB
+#define TG_G2_SUB 1  // epilogue sync groups (A/B: 1.87-1.89 vs 1.89-1.92 ms): 1 = two 2-warp groups per lane quarter (16 rows,
+                     // tcgen05.ld 16x32bx2), 0 = one 4-warp group per quarter (32 rows, 32x32b)
+#endif
+#ifndef TG_G2_ROWPTR
+#define TG_G2_ROWPTR 0  // store-path row pointer cached per tile row (A/B: 1.86 vs 1.83 ms; 0 recomputes per tile)
+#endif
+#if TG_G2_ROWPTR && !TG_G2_L2
+#error "TG_G2_ROWPTR assumes the .cs stores of TG_G2_L2"
+#endif
+#ifndef TG_G2_BULK
+#define TG_G2_BULK 0  // 1: non-masked tiles leave through 512-byte cp.async.bulk row stores (A/B: 1.95 vs 1.84 ms)
+#endif
+#if TG_G2_SUB
+static_assert(kG2EpiWarps == 16, "sub-group epilogue: 4 warps per lane quarter");
+// named barrier of the 2 epilogue warps of sub-group g (ids 1..8): 16 TMEM lanes
+__device__ __forceinline__ void g2_bar_quarter(uint32_t g) {
+    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(64) : "memory");
+}
+#else
 // named barrier of the 4 epilogue warps of TMEM lane quarter q (ids 1..4)
 __device__ __forceinline__ void g2_bar_quarter(uint32_t q) {
     asm volatile("bar.sync %0, %1;" ::"r"(q + 1), "n"(32 * (kG2EpiWarps / 4)) : "memory");
+}
+#endif
+
+// 16 TMEM lanes x 2 column halves: thread t < 16 reads lane base + t, columns
+// c .. c + N - 1; thread t >= 16 lane base + t - 16, columns c + 32 ..
+__device__ __forceinline__ void g2_ld32x2(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], 32;"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void g2_ld4x2(uint32_t taddr, uint32_t* v) {
+    asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x4.b32 {%0,%1,%2,%3}, [%4], 32;"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr));
 }
 
 __device__ __forceinline__ float g2_dist(uint32_t accbits, float ni, float nj, float m2, float cj = 1.0f) {
@@ -698,7 +738,7 @@ __device__ __forceinline__ float g2_dist(uint32_t accbits, float ni, float nj, f
     return dd;
 }
 
-__global__ void __launch_bounds__(kG2Threads, 1)
+__global__ void __launch_bounds__(kG2Threads, 1)  // 96 registers: 5 warps x 96 x 32 fit one SMSP's 16 K
     gram2_edm_kernel(const __grid_constant__ Gram2Geom g, const uint8_t* __restrict__ opA,
                      const uint8_t* __restrict__ opB, const float* __restrict__ norms,
                      const float* __restrict__ facs, const unsigned int* __restrict__ bits,
@@ -847,13 +887,37 @@ __global__ void __launch_bounds__(kG2Threads, 1)
         const int sh = g2_scale_exp(__ldg(bits));
         const float m2g = -2.0f * exp2f((float)(-2 * sh));
         // quarter staging tile: row slot r (= TMEM lane 32q + r) x 33 chunks (32 used)
+#if TG_G2_SUB
+        // sub-group sg = w4 / 2 of quarter q owns TMEM lanes 32 q + 16 sg + [0, 16) (16 rows x 128
+        // columns, its own staging and named barrier, so the two sub-groups of a quarter -- which
+        // share one SMSP -- drift out of phase instead of running MUFU / staging / stores in
+        // lockstep); warp m = w4 % 2 of it loads columns 64 m + [0, 64): thread t the row of lane
+        // t % 16, columns 64 m + 32 (t / 16) + [0, 32)
+        const uint32_t sg = w4 >> 1, m = w4 & 1;
+        const uint32_t cbase = 64 * m + 32 * (lane >> 4);
+        const uint32_t bq = 2 * q + sg;  // barrier / staging group
+        float4* qbuf = reinterpret_cast<float4*>(sE + bq * 2 * kG2EpiBytes) - 16 * sg * kG2QChunks;
+        const uint32_t r_lane = g2_perm(32 * q + 16 * sg + (lane & 15));
+        float4* my = qbuf + (16 * sg + (lane & 15)) * kG2QChunks + cbase / 4;
+#else
+        const uint32_t cbase = WCOLS * w4, bq = q;
         float4* qbuf = reinterpret_cast<float4*>(sE + q * EPW * kG2EpiBytes);
         const uint32_t r_lane = g2_perm(32 * q + lane);  // compute phase: lane = TMEM lane
         float4* my = qbuf + lane * kG2QChunks + (WCOLS / 4) * w4;
+#endif
         float4* out4 = reinterpret_cast<float4*>(out);
-        const uint32_t cw = WCOLS * w4 + s;  // first owned column of this warp, relative to the tile
+        const uint32_t cw = cbase + s;  // first owned column of this thread, relative to the tile
         const uint32_t rb0 = g2_perm(32 * q), rb1 = g2_perm(32 * q + 1);  // tile rows of slots 0, 1 (+8 per 2 slots)
 
+#if TG_G2_ROWPTR
+        uint32_t prow_i = ~0u;  // tile row of the cached row-slot pointer
+        float4* prow0 = out4;   // row slot 0 at column s of the tile row's column tile 0
+        uint32_t pd1 = 0, rd0 = 0, rd1 = 0;  // slot 1 - slot 0 (chunks); rows x + 8: + 2x + 9 chunks
+#endif
+#if TG_G2_BULK
+        uint64_t pol_ef;  // packed output: L2 evict-first
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
+#endif
         Coord c = ltm_map(tb, kReciprocal, true);
         uint32_t it = 0;
         for (uint64_t lam = tb; lam < te; ++lam, ++it) {
@@ -863,18 +927,25 @@ __global__ void __launch_bounds__(kG2Threads, 1)
             const float* nslot = reinterpret_cast<const float*>(sN + ns * kG2NormSlot);
             G2W(6, g2_wait_sleep(BAR(NF + ns), (it / kG2NormSlots) & 1));
             const float ni = nslot[kG2NormRowOff / 4 + r_lane];
-            const float4* nb4 = reinterpret_cast<const float4*>(nslot + WCOLS * w4);  // norms of loaded columns
-            const float4* cb4 = reinterpret_cast<const float4*>(nslot + kG2FacOff / 4 + WCOLS * w4);  // their 2^-s_j
+            const float4* nb4 = reinterpret_cast<const float4*>(nslot + cbase);  // norms of loaded columns
+            const float4* cb4 = reinterpret_cast<const float4*>(nslot + kG2FacOff / 4 + cbase);  // their 2^-s_j
             const float m2 = wide ? -2.0f * nslot[(kG2FacOff + kG2NormRowOff) / 4 + r_lane] : m2g;
             G2W(7, g2_wait_sleep(BAR(AF + buf), (it / kG2Acc) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const bool head = c.j == 0 && w4 == 0 && s > 0;  // warp-uniform: columns [0, s) of tile (i, 0)
             uint32_t v[WCOLS + 4];
+#if TG_G2_SUB
+            const bool head = c.j == 0 && m == 0 && s > 0;  // warp-uniform: columns [0, s) of tile (i, 0)
+            const uint32_t taddr = tmem + ((32 * q + 16 * sg) << 16) + buf * kG2AccStride + 64 * m;
+            g2_ld32x2(taddr + s, v);
+            if (head) g2_ld4x2(taddr, v + WCOLS);  // head columns 0..3 (threads t < 16)
+#else
+            const bool head = c.j == 0 && w4 == 0 && s > 0;  // warp-uniform: columns [0, s) of tile (i, 0)
             const uint32_t taddr = tmem + ((32 * q) << 16) + buf * kG2AccStride + WCOLS * w4;
             // owned columns s + WCOLS w4 + [0, WCOLS) (tcgen05.ld at the column offset)
 #pragma unroll
             for (int h = 0; h < NH; ++h) g2_ld32(taddr + 32 * h + s, v + 32 * h);
             if (head) g2_ld4(taddr, v + WCOLS);  // head columns 0..3
+#endif
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
@@ -922,26 +993,67 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                 for (int p = 0; p < WCOLS; ++p)
                     if (rj + cw + p == i) dv[p] = 0.0f;
             }
-            if (head && i < g.n && i >= g.r0 && i < g.r1) {
+            if (head && cbase == 0 && i < g.n && i >= g.r0 && i < g.r1) {
                 float* rowp = out + (i * (i + 1) / 2 - g.e_base);
                 const float nhv[3] = {nh0, nh1, nh2};
 #pragma unroll
                 for (uint32_t p = 0; p < 3; ++p)
                     if (p < s && p <= i) rowp[p] = (p == i) ? 0.0f : g2_dist(v[WCOLS + p], ni, nhv[p], m2, ch[p]);
             }
-            g2_bar_quarter(q);  // the quarter's previous tile is fully read
+#if TG_G2_BULK
+            // the bulk stores issued from this lane have finished reading the staging rows
+            if (lane < WROWS) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
+            g2_bar_quarter(bq);  // the group's previous tile is fully read
 #pragma unroll
             for (int cc = 0; cc < WCOLS / 4; ++cc)
                 my[cc] = make_float4(dv[4 * cc], dv[4 * cc + 1], dv[4 * cc + 2], dv[4 * cc + 3]);
+#if TG_G2_BULK
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging visible to the bulk copies
+#endif
             const Coord cn = c;
             g2_next(c);
-            g2_bar_quarter(q);  // the quarter's 32 rows x 32 chunks are staged
+            g2_bar_quarter(bq);  // the group's rows x 32 chunks are staged
             // warp w4 stores row slots WROWS w4 .. + WROWS, one 512-byte row segment per
             // instruction: slot 2 r2 + b (relative) is tile row 4 WROWS w4 + 8 r2 + rb_b
             const float4* src = qbuf + WROWS * w4 * kG2QChunks + lane;
+#if TG_G2_BULK
             if (!special) {
+                // lane r < WROWS: one 512-byte bulk copy (TMA engine) of row slot r, so the
+                // staging read and the global store leave the LSU / MIO path
+                if (lane < WROWS) {
+                    const uint64_t x = ri + 4 * WROWS * w4 + 8 * (lane >> 1) + ((lane & 1) ? rb1 : rb0);
+                    const float* dst = out + (x * (x + 1) / 2 + rj + s - g.e_base);
+                    asm volatile(
+                        "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], 512, %2;\n\t"
+                        "cp.async.bulk.commit_group;" ::"l"(dst),
+                        "r"(smem_u32(qbuf + (WROWS * w4 + lane) * kG2QChunks)), "l"(pol_ef)
+                        : "memory");
+                }
+            } else if (false) {
+#else
+            if (!special) {
+#endif
                 // chunk index of (row x, column rj + s) is (T(x) + rj + s - e_base) / 4;
                 // rows x + 8: + (8x + 36) / 4 = 2x + 9
+#if TG_G2_ROWPTR
+                // row-slot pointers and row offsets depend only on the tile row: recomputed when
+                // it changes, moved by 32 chunks per column tile (T(x) + s - e_base = 0 mod 4)
+                if ((uint32_t)cn.i != prow_i) {
+                    prow_i = (uint32_t)cn.i;
+                    const uint64_t x0 = ri + 4 * WROWS * w4 + rb0, x1 = ri + 4 * WROWS * w4 + rb1;
+                    prow0 = out4 + ((x0 * (x0 + 1) / 2 + s - g.e_base) >> 2) + lane;
+                    pd1 = (uint32_t)((x1 * (x1 + 1) / 2 - x0 * (x0 + 1) / 2) >> 2);  // x1 > x0, same shift
+                    rd0 = 2 * (uint32_t)x0 + 9;
+                    rd1 = 2 * (uint32_t)x1 + 9;
+                }
+                float4* p0 = prow0 + 32 * cn.j;
+#pragma unroll
+                for (int r2 = 0; r2 < WROWS / 2; ++r2) {
+                    __stcs(p0 + (uint32_t)(r2 * rd0 + 8 * r2 * (r2 - 1)), src[(2 * r2) * kG2QChunks]);
+                    __stcs(p0 + (uint32_t)(pd1 + r2 * rd1 + 8 * r2 * (r2 - 1)), src[(2 * r2 + 1) * kG2QChunks]);
+                }
+#else
                 const uint64_t colb = rj + s - g.e_base;
                 const uint64_t x0 = ri + 4 * WROWS * w4 + rb0, x1 = ri + 4 * WROWS * w4 + rb1;
                 float4* p0 = out4 + ((x0 * (x0 + 1) / 2 + colb) >> 2) + lane;
@@ -957,6 +1069,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                     p1[(uint32_t)(r2 * d1 + 8 * r2 * (r2 - 1))] = src[(2 * r2 + 1) * kG2QChunks];
 #endif
                 }
+#endif
             } else {
                 const uint64_t col0 = cn.j * kGT + s + 4 * lane;  // first column of this lane's chunk
 #pragma unroll 1
@@ -974,6 +1087,9 @@ __global__ void __launch_bounds__(kG2Threads, 1)
                 }
             }
         }
+#if TG_G2_BULK
+        if (lane < WROWS) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
     }
 #if TG_G2_PROF
     if (lane == 0 && (warp <= 2)) {
