@@ -691,6 +691,9 @@ __device__ __forceinline__ void g2_epi(const uint32_t* v, const float4* nb4, con
 #define TG_G2_SUB 1  // epilogue sync groups (A/B: 1.87-1.89 vs 1.89-1.92 ms): 1 = two 2-warp groups per lane quarter (16 rows,
                      // tcgen05.ld 16x32bx2), 0 = one 4-warp group per quarter (32 rows, 32x32b)
 #endif
+#ifndef TG_G2_CS
+#define TG_G2_CS 1  // interior row stores .cs (evict-first); 0: default caching (A/B: 1.89 vs 1.87 ms)
+#endif
 #ifndef TG_G2_ROWPTR
 #define TG_G2_ROWPTR 0  // store-path row pointer cached per tile row (A/B: 1.86 vs 1.83 ms; 0 recomputes per tile)
 #endif
@@ -1061,7 +1064,7 @@ __global__ void __launch_bounds__(kG2Threads, 1)  // 96 registers: 5 warps x 96 
                 const uint32_t d0 = 2 * (uint32_t)x0 + 9, d1 = 2 * (uint32_t)x1 + 9;
 #pragma unroll
                 for (int r2 = 0; r2 < WROWS / 2; ++r2) {
-#if TG_G2_L2
+#if TG_G2_L2 && TG_G2_CS
                     __stcs(p0 + (uint32_t)(r2 * d0 + 8 * r2 * (r2 - 1)), src[(2 * r2) * kG2QChunks]);
                     __stcs(p1 + (uint32_t)(r2 * d1 + 8 * r2 * (r2 - 1)), src[(2 * r2 + 1) * kG2QChunks]);
 #else
